@@ -1,0 +1,215 @@
+/* b200lu — C ABI of the B200-native (sm_100a, FP64) refactorize + solve path.
+ *
+ * This is the drop-in boundary for ONE path of the reference library `rlu`
+ * (arXiv 2306.14337 restatement): value scatter -> pivot-free numeric
+ * (re)factorization -> L/U triangular solves -> SpMV + FGMRES refinement, on a
+ * fixed sparsity pattern whose symbolic analysis (AMD ordering, optional MC64
+ * matching/scaling, fill pattern, scatter map) was produced by the reference's
+ * own host code and is consumed here bit-exact.
+ *
+ * Each entry point names the reference interface it replaces. Reference paths
+ * are relative to the reference tree's proj/ directory.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; int64 indices and float64 values, exactly
+ *     the reference's index_t / double (include/rlu/sparse.hpp:10-11);
+ *   - `on_device` != 0 means the vector/value pointers are device pointers on
+ *     the handle's device (no copy); 0 means host pointers (copied on the
+ *     handle's stream, the call returns after the result is on the host);
+ *   - every call on one handle must be serialised by the caller (the reference
+ *     contract, include/rlu/numeric.hpp:19-21); distinct handles are
+ *     independent;
+ *   - no device allocation happens after b200lu_create (the reference's
+ *     no-allocation-after-warm-up contract, include/rlu/trisolve.hpp:31-33);
+ *   - there is NO CPU fallback: without a CUDA device every compute entry
+ *     point returns B200LU_NO_DEVICE.
+ */
+#ifndef B200LU_H
+#define B200LU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct b200lu_handle b200lu_handle;
+
+/* Mirrors the reference's exception types (include/rlu/errors.hpp:11-54). */
+typedef enum {
+  B200LU_OK = 0,
+  B200LU_ZERO_PIVOT = 1,       /* rlu::ZeroPivotError{row}; see failed_row */
+  B200LU_PATTERN_MISMATCH = 2, /* rlu::PatternMismatchError */
+  B200LU_DIMENSION = 3,        /* rlu::DimensionError */
+  B200LU_INVALID_FACTORS = 4,  /* rlu::Error("...: factors are not valid"), src/trisolve.cpp:20 */
+  B200LU_CUDA_ERROR = 5,
+  B200LU_INVALID_ARGUMENT = 6,
+  B200LU_NO_DEVICE = 7
+} b200lu_status;
+
+/* Borrowed, read-only image of rlu::SymbolicFactors
+ * (include/rlu/symbolic.hpp:48-59). Only read during b200lu_create. */
+typedef struct {
+  int64_t n;
+  int64_t nnz_factors;              /* combined_pattern.nnz() */
+  int64_t nnz_source;               /* scatter_map.size() == nnz(A) */
+  const int64_t* row_offsets;       /* combined_pattern.row_offsets, n+1 */
+  const int64_t* col_indices;       /* combined_pattern.col_indices, nnz_factors */
+  const int64_t* diag_pos;          /* n */
+  const int64_t* scatter_map;       /* nnz_source */
+  const double* scatter_scale;      /* nnz_source */
+  const int64_t* amd_forward;       /* amd.forward, n */
+  const int64_t* col_perm_forward;  /* match->col_perm.forward, n; NULL when match is absent */
+  const double* row_scale;          /* match->scaling.row_scale, n; NULL when match is absent */
+  const double* col_scale;          /* match->scaling.col_scale, n; NULL when match is absent */
+  const int64_t* source_row_offsets; /* source_pattern.row_offsets, n+1 */
+  const int64_t* source_col_indices; /* source_pattern.col_indices, nnz_source */
+} b200lu_symbolic_view;
+
+/* rlu::FactorOptions (include/rlu/numeric.hpp:12-15); ExecPolicy is CPU-specific and has no
+ * device counterpart. */
+typedef struct {
+  double pivot_floor; /* |u_ii| at or below this fails the row; reference default 1e-30 */
+  int device;         /* CUDA device ordinal */
+  void* stream;       /* cudaStream_t to run on; NULL = the handle creates its own */
+  int refine_capacity; /* largest RefineConfig.max_iterations this handle will see (Krylov storage); 0 = 20 */
+  int reserved;
+} b200lu_options;
+
+/* rlu::RefineConfig (include/rlu/refine.hpp:13-17) */
+typedef struct {
+  int max_iterations; /* default 20 */
+  double tolerance;   /* default 1e-14 */
+} b200lu_refine_config;
+
+/* rlu::RefineOutcome (include/rlu/refine.hpp:19-24); x is returned through the call. */
+typedef struct {
+  int iterations;
+  int converged;
+  int history_len;
+  double residual_history[66]; /* [true initial, estimates...]; capacity max_iterations+1 <= 65 */
+} b200lu_refine_outcome;
+
+/* Derived-schedule facts, for reports and the roofline arithmetic. */
+typedef struct {
+  int64_t n, nnz_factors, nnz_source;
+  int64_t nnz_lower;        /* strict-lower slots == number of (row, pivot) pairs */
+  int64_t update_pairs;     /* sum over pivots of the pivot row's upper length */
+  int64_t lower_levels;     /* dependency levels of L (== levels of the factorization) */
+  int64_t upper_levels;
+  int64_t max_row_len;
+  int64_t big_rows;         /* rows handled by the per-CTA wide slot */
+  int64_t device_bytes;     /* total device memory owned by the handle */
+  int64_t alloc_events;     /* device allocations performed so far (constant after create) */
+} b200lu_stats;
+
+void b200lu_default_options(b200lu_options* opt);
+const char* b200lu_status_string(b200lu_status s);
+const char* b200lu_last_error(const b200lu_handle* h); /* "" when none */
+int b200lu_device_count(void);
+
+/* NumericFactors::NumericFactors (src/numeric.cpp:8-12): uploads the int32 pattern, diag_pos,
+ * scatter map/scale, permutations and scalings; derives the level schedules and the update
+ * destination table; allocates value, solve and refinement workspaces once. */
+b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_options* opt,
+                            b200lu_handle** out);
+void b200lu_destroy(b200lu_handle* h);
+
+/* pattern_equal(A, sym.source_pattern) guard of scatter_values (src/numeric.cpp:15-17,
+ * src/sparse.cpp pattern_equal). Host-side; returns B200LU_PATTERN_MISMATCH on any difference. */
+b200lu_status b200lu_check_pattern(const b200lu_handle* h, int64_t n, const int64_t* row_offsets,
+                                   const int64_t* col_indices);
+
+/* reset_values (src/numeric.cpp:75-77) == scatter_values (14-23) without the pattern guard:
+ * a_values is nnz_source doubles in source-CSR order. Also keeps A's values on the device
+ * as the operator for SpMV / refinement. Leaves the factors invalid until factorized. */
+b200lu_status b200lu_reset_values(b200lu_handle* h, const double* a_values, int on_device);
+
+/* factorize_scattered (src/numeric.cpp:79 -> eliminate 27-58). On a pivot with
+ * |u_ii| <= pivot_floor returns B200LU_ZERO_PIVOT and *failed_row = the lowest failing
+ * row of the permuted matrix; the factors stay invalid. failed_row may be NULL. */
+b200lu_status b200lu_factorize_scattered(b200lu_handle* h, int64_t* failed_row);
+
+/* refactorize (src/numeric.cpp:70-73) == reset_values + factorize_scattered. Also serves
+ * factorize (62-68) on a fresh handle. */
+b200lu_status b200lu_refactorize(b200lu_handle* h, const double* a_values, int on_device,
+                                 int64_t* failed_row);
+
+/* NumericFactors::valid / generation (include/rlu/numeric.hpp:25-26). */
+int b200lu_valid(const b200lu_handle* h);
+uint64_t b200lu_generation(const b200lu_handle* h);
+
+/* NumericFactors::values (include/rlu/numeric.hpp:24): nnz_factors doubles aligned to the
+ * combined pattern. After reset_values and before factorization this is the scattered
+ * matrix, exactly as in the reference. set_values mirrors tests that craft a factor
+ * object by hand (tests/test_trisolve.cpp:171-184). */
+b200lu_status b200lu_get_values(b200lu_handle* h, double* host_out);
+b200lu_status b200lu_set_values(b200lu_handle* h, const double* host_in, int valid);
+/* Device pointer to the factor values (borrowed; valid while the handle lives). */
+const double* b200lu_values_device(const b200lu_handle* h);
+
+/* lower_solve / upper_solve (src/trisolve.cpp:72-88 -> lower_core 28-42, upper_core 46-68),
+ * in the permuted space. `len` is checked against n (DimensionError). upper_solve reports an
+ * exactly zero diagonal as B200LU_ZERO_PIVOT with *failed_row = that row. */
+b200lu_status b200lu_lower_solve(b200lu_handle* h, int64_t len, const double* y, double* x,
+                                 int on_device);
+b200lu_status b200lu_upper_solve(b200lu_handle* h, int64_t len, const double* y, double* x,
+                                 int on_device, int64_t* failed_row);
+
+/* solve_system (src/trisolve.cpp:90-119): x = D_c Q P^T U^-1 L^-1 P D_r b. */
+b200lu_status b200lu_solve(b200lu_handle* h, int64_t len, const double* b, double* x,
+                           int on_device, int64_t* failed_row);
+
+/* spmv (src/sparse.cpp:128-143) and relative_residual (283-288) with A = the matrix whose
+ * values were last given to reset_values/refactorize. */
+b200lu_status b200lu_spmv(b200lu_handle* h, const double* x, double* y, int on_device);
+b200lu_status b200lu_relative_residual(b200lu_handle* h, const double* x, const double* b,
+                                       int on_device, double* out);
+
+/* fgmres_refine (src/refine.cpp:39-142) with A as above and the preconditioner
+ * solve_system(factors, .) — the pairing cli::solve_sequence uses (src/cli.cpp:121-135).
+ * use_preconditioner == 0 selects the identity operator (tests/test_refine.cpp:31).
+ * x0 and x_out may alias. Never fails for non-convergence (include/rlu/refine.hpp:41-42). */
+b200lu_status b200lu_refine_fgmres(b200lu_handle* h, const double* b, const double* x0,
+                                   double* x_out, int on_device, int use_preconditioner,
+                                   const b200lu_refine_config* cfg, b200lu_refine_outcome* outcome);
+
+/* classic_refine (src/refine.cpp:150-188). */
+b200lu_status b200lu_refine_classic(b200lu_handle* h, const double* b, const double* x0,
+                                    double* x_out, int on_device, int use_preconditioner,
+                                    const b200lu_refine_config* cfg, b200lu_refine_outcome* outcome);
+
+b200lu_status b200lu_get_stats(const b200lu_handle* h, b200lu_stats* out);
+/* Host-only (needs no device): validates a symbolic view and derives the device schedule the
+ * way b200lu_create does — the level orders that replace SyncFreeScheduler's ascending claim
+ * order (include/rlu/schedule.hpp:49-79) and the per-row update-pair offsets. Any of the three
+ * output arrays may be NULL. lower_order / upper_order: n int32; pair_row_ptr: n+1 int64. */
+b200lu_status b200lu_schedule_probe(const b200lu_symbolic_view* sym, b200lu_stats* stats,
+                                    int32_t* lower_order, int32_t* upper_order,
+                                    int64_t* pair_row_ptr, char* error_buf, int error_buf_len);
+/* Optional device-side phase timing: CUDA events recorded on the handle's stream around each
+ * kernel, the counterpart of the steady_clock phase timers of cli::solve_sequence
+ * (src/cli.cpp:105-132; fields scatter_ms / factor_ms / trisolve_ms / refine_ms of
+ * SystemRecord, include/rlu/report.hpp:19-22). ms_out / count_out hold B200LU_NUM_PHASES
+ * entries: accumulated kernel milliseconds and launch counts per phase since the last reset. */
+enum {
+  B200LU_PHASE_SCATTER = 0, /* K1 */
+  B200LU_PHASE_FACTOR = 1,  /* K2 */
+  B200LU_PHASE_LOWER = 2,   /* K3, L sweep */
+  B200LU_PHASE_UPPER = 3,   /* K3, U sweep */
+  B200LU_PHASE_PERMUTE = 4, /* solve_system prologue / epilogue */
+  B200LU_PHASE_SPMV = 5,    /* K4: SpMV / fused residual */
+  B200LU_PHASE_VECTOR = 6,  /* K4: dot, projection, axpy, scale */
+  B200LU_NUM_PHASES = 7
+};
+b200lu_status b200lu_set_timing(b200lu_handle* h, int enabled);
+b200lu_status b200lu_get_phase_times(b200lu_handle* h, double* ms_out, int64_t* count_out, int reset);
+/* Number of kernels this handle has launched since creation (bench.py's gpu_launches). */
+uint64_t b200lu_launch_count(const b200lu_handle* h);
+/* Blocks until everything queued on the handle's stream has finished. */
+b200lu_status b200lu_synchronize(b200lu_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200LU_H */

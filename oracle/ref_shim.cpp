@@ -307,6 +307,11 @@ void rluref_numeric_set_exec(void* hp, int parallel, int workers) {
   h->exec = make_exec(parallel, workers);
   h->nf->options.exec = h->exec;
 }
+// Execution policy of the solve phases only (solve_system takes its own ExecPolicy,
+// include/rlu/trisolve.hpp:36); rluref_numeric_set_exec sets both.
+void rluref_numeric_set_solve_exec(void* hp, int parallel, int workers) {
+  static_cast<NumHandle*>(hp)->exec = make_exec(parallel, workers);
+}
 int rluref_reset_values(void* h, void* A) {
   return guarded([&] { reset_values(*static_cast<NumHandle*>(h)->nf, *static_cast<CsrMatrix*>(A)); });
 }

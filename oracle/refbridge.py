@@ -96,6 +96,7 @@ def lib():
     sig("rluref_numeric_create", vp, vp, dbl, i32, i32)
     sig("rluref_numeric_destroy", None, vp)
     sig("rluref_numeric_set_exec", None, vp, i32, i32)
+    sig("rluref_numeric_set_solve_exec", None, vp, i32, i32)
     sig("rluref_reset_values", i32, vp, vp)
     sig("rluref_factorize_scattered", i32, vp)
     sig("rluref_refactorize", i32, vp, vp)
@@ -376,6 +377,10 @@ class RefNumeric:
 
     def set_exec(self, parallel: bool, workers=0):
         lib().rluref_numeric_set_exec(self._h, 1 if parallel else 0, workers)
+
+    def set_solve_exec(self, parallel: bool, workers=0):
+        """ExecPolicy handed to solve_system only (include/rlu/trisolve.hpp:36)."""
+        lib().rluref_numeric_set_solve_exec(self._h, 1 if parallel else 0, workers)
 
     def reset_values(self, A: RefCsr):
         _check(lib().rluref_reset_values(self._h, A._h))

@@ -1,0 +1,19 @@
+"""b200lu — B200-native (sm_100a, FP64 CUDA) refactorize + solve path for fixed-pattern KKT sequences.
+
+Drop-in for the reference library's numeric / triangular-solve / refinement entry points; the
+reference's host-side symbolic analysis is consumed as-is. See include/b200lu.h for the C ABI and
+DESIGN.md for the kernels.
+"""
+from .solver import (CsrMatrix, DeviceError, DimensionError, Error, FactorOptions, NumericFactors,
+                     PatternMismatchError, RefineConfig, RefineOutcome, SymbolicFactors,
+                     ZeroPivotError, classic_refine, factorize, factorize_scattered, fgmres_refine,
+                     lower_solve, refactorize, relative_residual, reset_values, scatter_values,
+                     solve_system, spmv, upper_solve)
+
+__all__ = [
+    "CsrMatrix", "DeviceError", "DimensionError", "Error", "FactorOptions", "NumericFactors",
+    "PatternMismatchError", "RefineConfig", "RefineOutcome", "SymbolicFactors", "ZeroPivotError",
+    "classic_refine", "factorize", "factorize_scattered", "fgmres_refine", "lower_solve",
+    "refactorize", "relative_residual", "reset_values", "scatter_values", "solve_system", "spmv",
+    "upper_solve",
+]

@@ -1,0 +1,99 @@
+"""ctypes binding of the C ABI in include/b200lu.h (libb200lu.so, built in-tree by __graft_entry__.build()).
+
+There is no fallback: if the CUDA library is missing, importing the solver raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libb200lu.so")
+
+OK, ZERO_PIVOT, PATTERN_MISMATCH, DIMENSION, INVALID_FACTORS, CUDA_ERROR, INVALID_ARGUMENT, NO_DEVICE = range(8)
+
+i64, u64, dbl, i32, vp = C.c_int64, C.c_uint64, C.c_double, C.c_int, C.c_void_p
+
+
+class SymbolicView(C.Structure):
+    _fields_ = [("n", i64), ("nnz_factors", i64), ("nnz_source", i64),
+                ("row_offsets", vp), ("col_indices", vp), ("diag_pos", vp),
+                ("scatter_map", vp), ("scatter_scale", vp), ("amd_forward", vp),
+                ("col_perm_forward", vp), ("row_scale", vp), ("col_scale", vp),
+                ("source_row_offsets", vp), ("source_col_indices", vp)]
+
+
+class Options(C.Structure):
+    _fields_ = [("pivot_floor", dbl), ("device", i32), ("stream", vp), ("refine_capacity", i32),
+                ("reserved", i32)]
+
+
+class RefineConfig(C.Structure):
+    _fields_ = [("max_iterations", i32), ("tolerance", dbl)]
+
+
+class RefineOutcome(C.Structure):
+    _fields_ = [("iterations", i32), ("converged", i32), ("history_len", i32),
+                ("residual_history", dbl * 66)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, i64) for k in ("n", "nnz_factors", "nnz_source", "nnz_lower", "update_pairs",
+                                   "lower_levels", "upper_levels", "max_row_len", "big_rows",
+                                   "device_bytes", "alloc_events")]
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "b200lu_default_options": (None, [C.POINTER(Options)]),
+    "b200lu_status_string": (C.c_char_p, [i32]),
+    "b200lu_last_error": (C.c_char_p, [vp]),
+    "b200lu_device_count": (i32, []),
+    "b200lu_create": (i32, [C.POINTER(SymbolicView), C.POINTER(Options), C.POINTER(vp)]),
+    "b200lu_destroy": (None, [vp]),
+    "b200lu_check_pattern": (i32, [vp, i64, vp, vp]),
+    "b200lu_reset_values": (i32, [vp, vp, i32]),
+    "b200lu_factorize_scattered": (i32, [vp, C.POINTER(i64)]),
+    "b200lu_refactorize": (i32, [vp, vp, i32, C.POINTER(i64)]),
+    "b200lu_valid": (i32, [vp]),
+    "b200lu_generation": (u64, [vp]),
+    "b200lu_get_values": (i32, [vp, vp]),
+    "b200lu_set_values": (i32, [vp, vp, i32]),
+    "b200lu_values_device": (vp, [vp]),
+    "b200lu_lower_solve": (i32, [vp, i64, vp, vp, i32]),
+    "b200lu_upper_solve": (i32, [vp, i64, vp, vp, i32, C.POINTER(i64)]),
+    "b200lu_solve": (i32, [vp, i64, vp, vp, i32, C.POINTER(i64)]),
+    "b200lu_spmv": (i32, [vp, vp, vp, i32]),
+    "b200lu_relative_residual": (i32, [vp, vp, vp, i32, C.POINTER(dbl)]),
+    "b200lu_refine_fgmres": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig),
+                                   C.POINTER(RefineOutcome)]),
+    "b200lu_refine_classic": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig),
+                                    C.POINTER(RefineOutcome)]),
+    "b200lu_get_stats": (i32, [vp, C.POINTER(Stats)]),
+    "b200lu_schedule_probe": (i32, [C.POINTER(SymbolicView), C.POINTER(Stats), vp, vp, vp, C.c_char_p, i32]),
+    "b200lu_set_timing": (i32, [vp, i32]),
+    "b200lu_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
+    "b200lu_launch_count": (u64, [vp]),
+    "b200lu_synchronize": (i32, [vp]),
+}
+
+PHASES = ("scatter", "factor", "lower", "upper", "permute", "spmv", "vector")
+
+_lib = None
+
+
+def lib():
+    """Loads libb200lu.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: the CUDA library is the only implementation of this "
+                "path. Build it with `python -c 'import __graft_entry__ as g; g.build()'`.")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib

@@ -1,0 +1,58 @@
+// Shared device helpers for the b200lu kernels (sm_100a, FP64 SIMT).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b200lu {
+
+// "Not written yet" marker for values that other rows/CTAs wait on. A quiet NaN
+// with a payload no arithmetic instruction produces; a computed value that
+// happens to carry these bits is canonicalised before it is published
+// (publish()), so a waiter can never mistake data for the marker or hang on it.
+constexpr unsigned long long kPendingBits = 0xFFFA5A5AB200B200ull;
+constexpr unsigned long long kCanonicalNaN = 0x7FF8000000000000ull;
+
+__device__ __forceinline__ bool is_pending(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(v)) == kPendingBits;
+}
+
+// L2-coherent (gpu-scope relaxed) 8-byte load/store: the unit of inter-CTA
+// communication in the sync-free kernels. Each value is self-validating, so no
+// fence or separate ready flag is needed.
+__device__ __forceinline__ double ld_l2(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return __longlong_as_double(static_cast<long long>(v));
+}
+
+__device__ __forceinline__ void st_l2(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p),
+               "l"(static_cast<unsigned long long>(__double_as_longlong(v))));
+}
+
+__device__ __forceinline__ void publish(double* p, double v) {
+  if (is_pending(v)) v = __longlong_as_double(static_cast<long long>(kCanonicalNaN));
+  st_l2(p, v);
+}
+
+// Spins until *p has been published by its owner.
+__device__ __forceinline__ double wait_value(const double* p) {
+  double v = ld_l2(p);
+  while (is_pending(v)) {
+    __nanosleep(32);
+    v = ld_l2(p);
+  }
+  return v;
+}
+
+// a - b*c with two roundings (the reference's x86-64 baseline build has no FMA
+// contraction: src/numeric.cpp:44, src/trisolve.cpp:38,57).
+__device__ __forceinline__ double sub_prod(double a, double b, double c) {
+  return __dsub_rn(a, __dmul_rn(b, c));
+}
+__device__ __forceinline__ double add_prod(double a, double b, double c) {
+  return __dadd_rn(a, __dmul_rn(b, c));
+}
+
+}  // namespace b200lu

@@ -1,0 +1,199 @@
+// K1 value scatter and K2 numeric refactorization.
+#pragma once
+
+#include "common.cuh"
+
+namespace b200lu {
+
+// ------------------------------------------------------------------ K1 scatter
+//
+// Reference: scatter_values, src/numeric.cpp:19-22 — out.assign(nnzF, 0) then
+// out[scatter_map[k]] = A.values[k] * scatter_scale[k].
+//
+// One fused pass in gather form: slot s reads its source entry through the inverse map
+// (src_of_slot[s] == -1 marks a fill slot, which becomes exactly 0), so every store is
+// coalesced and no slot is written twice. The same pass re-arms `values` with the pending
+// marker that the refactorization kernel's waiters test for.
+__global__ void __launch_bounds__(256)
+scatter_kernel(int64_t nnz_factors, const int32_t* __restrict__ src_of_slot,
+               const double* __restrict__ a_values, const double* __restrict__ scatter_scale,
+               double* __restrict__ work, double* __restrict__ values) {
+  const double pending = __longlong_as_double(static_cast<long long>(kPendingBits));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < nnz_factors;
+       s += stride) {
+    const int32_t k = __ldg(src_of_slot + s);
+    double v = 0.0;
+    if (k >= 0) {
+      v = __ldg(a_values + k);
+      if (scatter_scale != nullptr) v = __dmul_rn(v, __ldg(scatter_scale + k));
+    }
+    work[s] = v;
+    values[s] = pending;
+  }
+}
+
+// --------------------------------------------------- update destination table
+//
+// For the pivot (i, d) — row i has a strict-lower entry in column d — every upper entry
+// (d, j) of row d updates slot (i, j). The reference finds that slot through
+// RowLookupTable::lookup (src/symbolic.cpp:73-93) once per update, every factorization.
+// The pattern is fixed, so the offsets are resolved ONCE here and streamed afterwards:
+// dest[pair_row_ptr[i] + running pair index] = offset of column j inside row i.
+template <typename DestT>
+__global__ void __launch_bounds__(256)
+build_dest_kernel(int32_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                  const int32_t* __restrict__ diag, const int64_t* __restrict__ pair_row_ptr,
+                  DestT* __restrict__ dest) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int32_t lo = row_ptr[i], dg = diag[i], hi = row_ptr[i + 1];
+    int64_t p = pair_row_ptr[i];
+    for (int32_t k = lo; k < dg; ++k) {
+      const int32_t d = col[k];
+      const int32_t dd = diag[d];
+      const int32_t m = row_ptr[d + 1] - dd - 1;
+      for (int32_t c = lane; c < m; c += 32) {
+        const int32_t j = col[dd + 1 + c];
+        // binary search for j in col[k+1, hi); the fill pattern is closed under row
+        // updates (src/numeric.cpp:43), so j is always present.
+        int32_t a = k + 1, b = hi - 1;
+        while (a < b) {
+          const int32_t mid = (a + b) >> 1;
+          if (col[mid] < j) a = mid + 1; else b = mid;
+        }
+        dest[p + c] = static_cast<DestT>(a - lo);
+      }
+      p += m;
+    }
+  }
+}
+
+// ------------------------------------------------------ K2 refactorization
+//
+// Reference: eliminate, src/numeric.cpp:27-58, driven by SyncFreeScheduler
+// (include/rlu/schedule.hpp:49-79).
+//
+// Row ownership is kept: one warp owns row i from start to finish and applies the pivots d
+// in ascending order, so every slot receives its updates in the reference's order and the
+// result is bit-identical to the sequential CPU run regardless of scheduling. What changes:
+//   * rows are claimed in dependency-level order from two queues (rows a warp slot can hold,
+//     and wide rows that use the CTA's wide slot), by persistent warps;
+//   * row i is staged in shared memory while its pivots are applied;
+//   * there are no ready flags: a finished row publishes its values into `values`, which K1
+//     armed with the pending marker; a consumer lane that needs u_dj simply waits on that
+//     8-byte value (Ginkgo's sentinel idea, applied to the factorization);
+//   * the column->slot lookup is the precomputed destination table.
+struct FactorArgs {
+  int32_t n;
+  int32_t n_small, n_big;
+  int32_t small_slot, big_slot;  // capacities in doubles
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const int32_t* diag;
+  const int32_t* small_rows;
+  const int32_t* big_rows;
+  const int64_t* pair_row_ptr;
+  const void* dest;
+  double* work;     // scattered input values (K1), also the in-place fallback for over-wide rows
+  double* values;   // published factors
+  double pivot_floor;
+  int32_t* counters;  // [0] small-queue ticket, [1] big-queue ticket
+  int32_t* failed_row;  // atomicMin target, initialised to INT32_MAX
+};
+
+template <typename DestT>
+__device__ __forceinline__ void factor_row(const FactorArgs& a, int32_t i, double* row, int lane) {
+  const int32_t lo = a.row_ptr[i], dg = a.diag[i], hi = a.row_ptr[i + 1];
+  const int32_t len = hi - lo, nl = dg - lo;
+  const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
+  const double* values = a.values;
+
+  if (row != a.work + lo) {
+    for (int32_t c = lane; c < len; c += 32) row[c] = a.work[lo + c];
+  }
+  __syncwarp();
+
+  int64_t p = a.pair_row_ptr[i];
+  for (int32_t k0 = 0; k0 < nl; k0 += 32) {
+    // Lane q of this chunk resolves the metadata of pivot k0+q; the walk below is sequential.
+    int32_t my_dd = 0, my_m = 0;
+    if (k0 + lane < nl) {
+      const int32_t d = __ldg(a.col + lo + k0 + lane);
+      my_dd = __ldg(a.diag + d);
+      my_m = __ldg(a.row_ptr + d + 1) - my_dd - 1;
+    }
+    const int32_t cnt = min(32, nl - k0);
+    for (int32_t q = 0; q < cnt; ++q) {
+      const int32_t dd = __shfl_sync(0xffffffffu, my_dd, q);
+      const int32_t m = __shfl_sync(0xffffffffu, my_m, q);
+      // Issue this lane's loads before waiting on anything.
+      double u0 = 0.0, u1 = 0.0;
+      int32_t s0 = 0, s1 = 0;
+      const bool h0 = lane < m, h1 = lane + 32 < m;
+      if (h0) { u0 = ld_l2(values + dd + 1 + lane); s0 = dest[p + lane]; }
+      if (h1) { u1 = ld_l2(values + dd + 33 + lane); s1 = dest[p + 32 + lane]; }
+      const double udiag = wait_value(values + dd);
+      const double alpha = row[k0 + q] / udiag;  // src/numeric.cpp:40
+      if (h0) {
+        while (is_pending(u0)) { __nanosleep(32); u0 = ld_l2(values + dd + 1 + lane); }
+        row[s0] = sub_prod(row[s0], alpha, u0);  // src/numeric.cpp:44
+      }
+      if (h1) {
+        while (is_pending(u1)) { __nanosleep(32); u1 = ld_l2(values + dd + 33 + lane); }
+        row[s1] = sub_prod(row[s1], alpha, u1);
+      }
+      for (int32_t c = lane + 64; c < m; c += 32) {
+        const double u = wait_value(values + dd + 1 + c);
+        const int32_t s = dest[p + c];
+        row[s] = sub_prod(row[s], alpha, u);
+      }
+      p += m;
+      __syncwarp();
+      if (lane == 0) row[k0 + q] = alpha;  // src/numeric.cpp:41
+    }
+    __syncwarp();
+  }
+
+  // src/numeric.cpp:48: the row completes (and is published) even when its pivot fails, so
+  // dependents never hang (include/rlu/schedule.hpp:29-33); the lowest failing row wins (82-87).
+  if (lane == 0 && fabs(row[nl]) <= a.pivot_floor) atomicMin(a.failed_row, i);
+  for (int32_t c = lane; c < len; c += 32) publish(a.values + lo + c, row[c]);
+}
+
+template <typename DestT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+factor_kernel(const FactorArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  double* small_slot = smem + static_cast<size_t>(w) * a.small_slot;
+  double* big_slot = smem + static_cast<size_t>(WARPS) * a.small_slot;
+
+  // Warp 0 of every CTA serves the wide-row queue first (it alone may use the wide slot).
+  if (w == 0) {
+    while (true) {
+      int32_t r = 0;
+      if (lane == 0) r = atomicAdd(a.counters + 1, 1);
+      r = __shfl_sync(0xffffffffu, r, 0);
+      if (r >= a.n_big) break;
+      const int32_t i = a.big_rows[r];
+      const int32_t len = a.row_ptr[i + 1] - a.row_ptr[i];
+      double* row = len <= a.big_slot ? big_slot : a.work + a.row_ptr[i];
+      factor_row<DestT>(a, i, row, lane);
+      __syncwarp();
+    }
+  }
+  while (true) {
+    int32_t r = 0;
+    if (lane == 0) r = atomicAdd(a.counters, 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= a.n_small) break;
+    factor_row<DestT>(a, a.small_rows[r], small_slot, lane);
+    __syncwarp();
+  }
+}
+
+}  // namespace b200lu
