@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Headline benchmark: refactorize + solve (+ FGMRES) per KKT system, systems/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl b200|reference]
+
+One "step" = one KKT system of the generated sequence taken through the hot path exactly as
+cli::solve_sequence does (reference proj/src/cli.cpp:105-135): value scatter, numeric
+refactorization, solve_system, FGMRES refinement. Inputs are the reference's own synthetic
+generator (gen_sequence, proj/src/kkt.cpp:94-207) and its host-side symbolic analysis, produced once
+before the timed region through the reference bridge (input fixture, not the measured path).
+
+  value   device-resident: values and rhs already in HBM, x stays in HBM.
+  e2e     same steps through the public API with HOST buffers: values + rhs copied H2D from pinned
+          memory and x copied D2H inside the timed region, every step.
+  --impl reference   the unmodified reference CPU implementation (oracle/_ref) on this box's cores.
+
+Under torchrun every rank runs the same workload on its own scenario (y_seed = 2 + rank: same
+pattern, different values) — weak scaling with no data-path collective; NCCL/gloo only carries the
+per-rank timings and residuals to rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (n, m, description)  — SURVEY §8d / BASELINE.json configs
+    "C1": (6300, 2700, "ACTIVSg200-shaped KKT, n+m=9000"),
+    "C2": (39000, 16700, "ACTIVSg2000-shaped KKT, n+m=55700"),
+    "C3": (166600, 71400, "ACTIVSg10k-shaped KKT, n+m=238000"),
+    "C4": (1120000, 480000, "ACTIVSg70k-shaped KKT, n+m=1600000"),
+}
+METRIC = "systems/sec (refactor+solve+FGMRES per KKT system)"
+UNIT = "systems/s"
+
+
+def algorithmic_bytes(n, nnz_a, nnz_f, fgmres_iters=1):
+    """SURVEY §8(d) compulsory-traffic model, int32 indices on the device."""
+    scatter = 12 * nnz_a + 8 * nnz_f
+    eliminate = 20 * nnz_f + 8 * n
+    solve = 12 * nnz_f + 76 * n
+    spmv = 12 * nnz_a + 20 * n
+    j = fgmres_iters
+    fgmres = (j + 2) * spmv + j * solve + 8 * n * (4 * sum(i + 1 for i in range(j)) + 6 * j + 4) if j else 2 * spmv
+    return dict(scatter=scatter, eliminate=eliminate, solve=solve, spmv=spmv, fgmres=fgmres,
+                total=scatter + eliminate + solve + fgmres)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(device_index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.strip().split(", ") for r in open(self.f.name) if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def reference_pass(num, seq, k, refine=True):
+    """One system through the reference with the best execution policy per phase (measured on this
+    host: scheduled_parallel helps eliminate, hurts the triangular solves — SURVEY §6)."""
+    return num.run_system(seq, k, refine=refine)
+
+
+def calibrate_reference(ref_sym, seq, rb):
+    """Times both ExecModes once and keeps the better one per phase (factor / solve)."""
+    threads = rb.max_threads()
+    num = rb.RefNumeric(ref_sym)
+    seq_run = num.run_system(seq, 0)
+    best = {"factor_parallel": False, "solve_parallel": False, "threads": threads,
+            "sequential": {k: float(seq_run[k]) for k in ("scatter_ms", "factor_ms", "trisolve_ms", "refine_ms")}}
+    if threads > 1:
+        num.set_exec(True, threads)
+        par_run = num.run_system(seq, 0)
+        best["parallel"] = {k: float(par_run[k]) for k in ("scatter_ms", "factor_ms", "trisolve_ms", "refine_ms")}
+        best["factor_parallel"] = bool(par_run["factor_ms"] < seq_run["factor_ms"])
+        best["solve_parallel"] = bool(par_run["trisolve_ms"] + par_run["refine_ms"]
+                                      < seq_run["trisolve_ms"] + seq_run["refine_ms"])
+    num.set_exec(best["factor_parallel"], threads)
+    num.set_solve_exec(best["solve_parallel"], threads)
+    return num, best
+
+
+def run_reference(args):
+    """--impl reference: the unmodified reference CPU path on this box's host cores."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from oracle import refbridge as rb
+    n, m, desc = WORKLOADS[args.workload]
+    seq = rb.RefSequence(n, m)
+    ref_sym = rb.RefSymbolic(seq.matrix(0), use_scaling=False, use_amd=True)
+    num, policy = calibrate_reference(ref_sym, seq, rb)
+    nsys = len(seq)
+    for w in range(args.warmup):
+        num.run_system(seq, w % nsys)
+    t0 = time.perf_counter()
+    phases = {"scatter_ms": 0.0, "factor_ms": 0.0, "trisolve_ms": 0.0, "refine_ms": 0.0}
+    worst = 0.0
+    for s in range(args.steps):
+        r = num.run_system(seq, s % nsys)
+        for k in phases:
+            phases[k] += r[k]
+        worst = max(worst, r["relres_final"])
+    wall = time.perf_counter() - t0
+    hot_ms = sum(phases.values()) / args.steps
+    value = 1000.0 / hot_ms
+    cores = policy["threads"]
+    sample = (f"{args.steps} systems of the {args.workload} sequence (k = 0..), one system per step; eliminate "
+              f"{'scheduled_parallel x' + str(cores) if policy['factor_parallel'] else 'sequential'}, solves "
+              f"{'scheduled_parallel x' + str(cores) if policy['solve_parallel'] else 'sequential'} (best mode per phase)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": hot_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {desc}; scatter+eliminate+solve_system+fgmres_refine per system "
+                               "(cli.cpp:105-135 clocks); reference CPU path", "n": seq.n, "nnz": seq.nnz,
+                   "nnz_factors": ref_sym.nnz_factors, "analysis": "use_scaling=false,use_amd=true"},
+        "phases_ms": {k: v / args.steps for k, v in phases.items()},
+        "wall_ms_per_step": 1000.0 * wall / args.steps, "worst_relres_final": worst,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+                         "calibration": policy},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_14337_b200 as rlu
+    from oracle import refbridge as rb  # input fixtures + CPU baseline arm only
+
+    rank, local_rank, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the b200lu path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    n, m, desc = WORKLOADS[args.workload]
+    # ---- input fixture (untimed): the reference's generator + host-side symbolic analysis
+    seq = rb.RefSequence(n, m, y_seed=2 + rank)
+    ref_sym = rb.RefSymbolic(seq.matrix(0), use_scaling=False, use_amd=True)
+    sym = rlu.SymbolicFactors.from_arrays(ref_sym.arrays())
+    ro, ci = seq.pattern()
+    nsys = len(seq)
+    N, nnz_a, nnz_f = seq.n, seq.nnz, ref_sym.nnz_factors
+
+    stream = torch.cuda.current_stream()
+    f = rlu.NumericFactors(sym, rlu.FactorOptions(device=local_rank, stream=stream.cuda_stream))
+    cfg = rlu.RefineConfig(args.refine_maxit, args.refine_tol)
+
+    host_vals = [torch.from_numpy(seq.values(k)).pin_memory() for k in range(nsys)]
+    host_rhs = [torch.from_numpy(seq.rhs(k)).pin_memory() for k in range(nsys)]
+    dev_vals = [v.cuda(non_blocking=True) for v in host_vals]
+    dev_rhs = [b.cuda(non_blocking=True) for b in host_rhs]
+    host_x = torch.empty(N, dtype=torch.float64).pin_memory()
+    dev_b = torch.empty(N, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    torch.cuda.synchronize()
+
+    # One CsrMatrix per system, built once: the pattern guard (pattern_equal) runs on the first
+    # submission of each object, in the warm-up, as it would for a caller that keeps its matrices.
+    dev_mats = [rlu.CsrMatrix(N, N, ro, ci, dev_vals[k]) for k in range(nsys)]
+    host_mats = [rlu.CsrMatrix(N, N, ro, ci, host_vals[k].numpy()) for k in range(nsys)]
+
+    def step_resident(k):
+        rlu.refactorize(f, dev_mats[k])
+        x = rlu.solve_system(f, dev_rhs[k])
+        if args.no_refine:
+            return x, 0
+        out = rlu.fgmres_refine(f, dev_rhs[k], x, cfg)
+        return out.x, out.iterations
+
+    def step_e2e(k):
+        # host values -> H2D inside refactorize; rhs H2D; x D2H — all on the handle's stream
+        rlu.refactorize(f, host_mats[k])
+        dev_b.copy_(host_rhs[k], non_blocking=True)
+        x = rlu.solve_system(f, dev_b)
+        its = 0
+        if not args.no_refine:
+            out = rlu.fgmres_refine(f, dev_b, x, cfg)
+            x, its = out.x, out.iterations
+        host_x.copy_(x, non_blocking=True)
+        stream.synchronize()
+        return host_x, its
+
+    def timed(step_fn, steps, warmup, sample_clocks):
+        for w in range(max(warmup, nsys)):  # every matrix object is submitted (and guarded) once
+            step_fn(w % nsys)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local_rank) if sample_clocks else None
+        f.set_timing(True)
+        launches0 = f.launch_count
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        iters = []
+        for s in range(steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the timed pair)
+            ev[s][0].record()
+            _, its = step_fn(s % nsys)
+            ev[s][1].record()
+            iters.append(its)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sampler else None
+        per_step = [a.elapsed_time(b) for a, b in ev]
+        phases = f.phase_times()
+        f.set_timing(False)
+        return sum(per_step), per_step, iters, phases, f.launch_count - launches0, clocks
+
+    total_ms, per_step, iters, phases, launches, clocks = timed(step_resident, args.steps, args.warmup, True)
+    e2e_total_ms, e2e_steps, _, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2), False)
+
+    # ---- parity spot check on the last system processed (oracle/reference as the checker only)
+    k_last = (args.steps - 1) % nsys
+    x_last, _ = step_resident(k_last)
+    relres = seq.matrix(k_last).relative_residual(x_last.cpu().numpy(), seq.rhs(k_last))
+
+    # ---- max over ranks
+    t = torch.tensor([total_ms, e2e_total_ms, relres], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max, e2e_ms_max, relres_max = (float(v) for v in t.cpu())
+
+    if rank == 0:
+        ms_per_step = total_ms_max / args.steps
+        value = world * args.steps / (total_ms_max / 1000.0)
+        e2e_value = world * args.steps / (e2e_ms_max / 1000.0)
+        med_iters = int(statistics.median(iters)) if iters else 0
+        ab = algorithmic_bytes(N, nnz_a, nnz_f, 0 if args.no_refine else max(med_iters, 0))
+        peak, peak_src = measured_peak()
+        fac_ms, fac_n = phases["factor"]
+        fac_avg_ms = fac_ms / max(fac_n, 1)
+        achieved = ab["eliminate"] / (fac_avg_ms * 1e-3) / 1e9 if fac_avg_ms > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload, {}).get("factor_kernel_dram_bytes")
+        st = f.stats
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{args.workload}: {desc}; one system per step per GPU: scatter + refactorize + "
+                            f"solve_system{'' if args.no_refine else ' + fgmres_refine(tol=%g)' % args.refine_tol}; "
+                            "10-system mu sequence, gen_sequence defaults, AMD-only analysis (KLU-style path)",
+                "n": N, "nnz": nnz_a, "nnz_factors": nnz_f, "update_pairs": st["update_pairs"],
+                "levels": st["lower_levels"], "scenario_per_rank": "y_seed = 2 + rank, shared pattern",
+                "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); "
+                      "the per-step working set (values + destination table) also exceeds the 126 MB L2",
+                "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks",
+            },
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms_max / args.steps,
+                    "h2d_bytes_per_step": 8 * nnz_a + 8 * N, "d2h_bytes_per_step": 8 * N,
+                    "note": "values + rhs from pinned host memory H2D and x D2H inside the timed region, through "
+                            "the public refactorize/solve_system/fgmres_refine calls"},
+            "gpu_launches": launches,
+            "phases_ms_per_step": {p: v[0] / args.steps for p, v in phases.items()},
+            "launches_per_step": {p: v[1] / args.steps for p, v in phases.items()},
+            "refine_iters_median": med_iters, "relres_final_max": relres_max,
+            "roofline": {
+                "kernel": "factor_kernel (K2 numeric refactorization)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
+                "bytes_model": "SURVEY 8(d): eliminate = 20*nnz(L+U) + 8*N per system, one system per launch",
+                "whole_step": {"algorithmic_bytes": ab["total"],
+                               "achieved_gbs": ab["total"] / (ms_per_step * 1e-3) / 1e9,
+                               "frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / peak},
+                "second_bound": f"critical path: {st['lower_levels']} dependency levels per sweep x 3 sweeps",
+            },
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            num, policy = calibrate_reference(ref_sym, seq, rb)
+            reps = max(1, args.cpu_reps)
+            tot = 0.0
+            for r in range(reps):
+                o = num.run_system(seq, r % nsys, refine=not args.no_refine, max_iterations=args.refine_maxit,
+                                   tolerance=args.refine_tol)
+                tot += o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"]
+            cpu_ms = tot / reps
+            line["cpu_baseline"] = {
+                "value": 1000.0 / cpu_ms, "unit": UNIT, "ms_per_system": cpu_ms, "cores": policy["threads"],
+                "kind": "reference",
+                "sample": f"{reps} systems of the same {args.workload} sequence through the unmodified reference "
+                          "(oracle/_ref), best ExecMode per phase after one calibration pass of each mode",
+                "calibration": policy}
+        print(json.dumps(line))
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-refine", action="store_true")
+    ap.add_argument("--refine-tol", type=float, default=1e-14)
+    ap.add_argument("--refine-maxit", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

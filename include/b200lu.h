@@ -73,8 +73,16 @@ typedef struct {
   int device;         /* CUDA device ordinal */
   void* stream;       /* cudaStream_t to run on; NULL = the handle creates its own */
   int refine_capacity; /* largest RefineConfig.max_iterations this handle will see (Krylov storage); 0 = 20 */
-  int reserved;
+  int flags;           /* B200LU_FLAG_* */
 } b200lu_options;
+
+/* Summation order of the U sweep (upper_core, src/trisolve.cpp:52-58). The L/U values, the L
+ * sweep and SpMV always reproduce the reference bit for bit. By default the U sweep folds each
+ * row from its last column to its first — the order in which its dependencies are produced on
+ * the device — which is deterministic but rounds the partial sums differently from the
+ * reference. With this flag it folds in the reference's ascending column order and
+ * upper_solve / solve_system are bit-identical to the CPU result, at a longer critical path. */
+#define B200LU_FLAG_STRICT_ORDER 1
 
 /* rlu::RefineConfig (include/rlu/refine.hpp:13-17) */
 typedef struct {

@@ -25,7 +25,7 @@ class SymbolicView(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("pivot_floor", dbl), ("device", i32), ("stream", vp), ("refine_capacity", i32),
-                ("reserved", i32)]
+                ("flags", i32)]
 
 
 class RefineConfig(C.Structure):
@@ -77,6 +77,7 @@ EXPORTS = {
     "b200lu_synchronize": (i32, [vp]),
 }
 
+FLAG_STRICT_ORDER = 1
 PHASES = ("scatter", "factor", "lower", "upper", "permute", "spmv", "vector")
 
 _lib = None

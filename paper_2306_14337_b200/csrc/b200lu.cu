@@ -12,6 +12,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -26,7 +27,6 @@ using namespace b200lu;
 namespace {
 
 constexpr int kFactorWarps = 8;
-constexpr int kSmallSlot = 512;        // doubles per warp slot
 constexpr int kMaxBigSlot = 20 * 1024; // doubles; wider rows fall back to in-place global updates
 constexpr int kReduceBlocks = 592;     // 4 per SM on a 148-SM part; fixed so sums are reproducible
 
@@ -36,8 +36,10 @@ __global__ void arm_factor_kernel(int32_t* counters, int32_t* failed_row) {
   *failed_row = INT_MAX;
 }
 __global__ void arm_solve_kernel(int32_t* counters, int32_t* failed_upper) {
-  counters[2] = 0;
-  counters[3] = 0;
+  counters[2] = 0;  // lower ticket
+  counters[3] = 0;  // upper ticket
+  counters[4] = 0;  // lower rows finished
+  counters[5] = 0;  // upper rows finished
   *failed_upper = -1;
 }
 
@@ -49,6 +51,7 @@ struct b200lu_handle {
   bool owns_stream = false;
   double pivot_floor = 1e-30;
   int refine_capacity = 20;
+  bool strict_order = false;  // U sweep folds in the reference's ascending column order
 
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
@@ -61,6 +64,9 @@ struct b200lu_handle {
   int32_t *d_small_rows = nullptr, *d_big_rows = nullptr, *d_lower_order = nullptr,
           *d_upper_order = nullptr;
   int64_t* d_pair_row_ptr = nullptr;
+  RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;      // triangular sweeps
+  FactorMeta *d_small_meta = nullptr, *d_big_meta = nullptr;    // refactorization queues
+  ScheduleTuning tune;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
   double* d_scatter_scale = nullptr;
@@ -71,7 +77,7 @@ struct b200lu_handle {
   double *d_a_vals = nullptr, *d_work = nullptr, *d_values = nullptr;
   double *d_w = nullptr, *d_t1 = nullptr, *d_t2 = nullptr;
   double *d_in = nullptr, *d_in2 = nullptr, *d_out = nullptr;  // host<->device staging
-  int32_t* d_counters = nullptr;  // [0,1] factor tickets, [2] lower, [3] upper
+  int32_t* d_counters = nullptr;  // [0,1] factor tickets, [2,3] lower/upper tickets, [4,5] rows finished
   int32_t* d_failed = nullptr;    // [0] factor (atomicMin), [1] upper (atomicMax)
   double* d_scal = nullptr;       // scalar results of reductions
   double* d_partials = nullptr;
@@ -185,16 +191,15 @@ b200lu_status launch_factor(H* h, int64_t* failed_row) {
   arm_factor_kernel<<<1, 1, 0, h->stream>>>(h->d_counters, h->d_failed);
   ST_TRY(check_launch(h, "arm_factor_kernel"));
   FactorArgs a;
-  a.n = static_cast<int32_t>(h->n);
   a.n_small = static_cast<int32_t>(h->sched.small_rows.size());
   a.n_big = static_cast<int32_t>(h->sched.big_rows.size());
-  a.small_slot = kSmallSlot;
+  a.small_slot = static_cast<int32_t>(h->tune.small_slot);
   a.big_slot = h->big_slot;
   a.row_ptr = h->d_row_ptr;
   a.col = h->d_col;
   a.diag = h->d_diag;
-  a.small_rows = h->d_small_rows;
-  a.big_rows = h->d_big_rows;
+  a.small_meta = h->d_small_meta;
+  a.big_meta = h->d_big_meta;
   a.pair_row_ptr = h->d_pair_row_ptr;
   a.dest = h->d_dest;
   a.work = h->d_work;
@@ -226,30 +231,34 @@ b200lu_status launch_factor(H* h, int64_t* failed_row) {
   return B200LU_OK;
 }
 
-TriArgs tri_args(H* h, const int32_t* order, const double* y, double* x, int counter_slot) {
+TriArgs tri_args(H* h, const RowMeta* meta, const double* y, double* x, int counter_slot) {
   TriArgs a;
   a.n = static_cast<int32_t>(h->n);
-  a.row_ptr = h->d_row_ptr;
+  a.meta = meta;
   a.col = h->d_col;
   a.diag = h->d_diag;
-  a.order = order;
   a.values = h->d_values;
   a.y = y;
   a.x = x;
   a.counter = h->d_counters + counter_slot;
+  a.finished = h->d_counters + counter_slot + 2;
   a.failed_row = h->d_failed + 1;
   return a;
 }
 
 b200lu_status launch_lower(H* h, const double* y, double* x) {
   PhaseScope ps(h, B200LU_PHASE_LOWER);
-  lower_kernel<<<h->tri_grid, 128, 0, h->stream>>>(tri_args(h, h->d_lower_order, y, x, 2));
-  return check_launch(h, "lower_kernel");
+  tri_kernel<false, false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 2));
+  return check_launch(h, "tri_kernel<lower>");
 }
 b200lu_status launch_upper(H* h, const double* y, double* x) {
   PhaseScope ps(h, B200LU_PHASE_UPPER);
-  upper_kernel<<<h->tri_grid, 128, 0, h->stream>>>(tri_args(h, h->d_upper_order, y, x, 3));
-  return check_launch(h, "upper_kernel");
+  if (h->strict_order) {
+    tri_kernel<true, false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 3));
+  } else {
+    tri_kernel<true, true><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 3));
+  }
+  return check_launch(h, "tri_kernel<upper>");
 }
 
 // Device-to-device solve_system (src/trisolve.cpp:90-119). Does not synchronise; an exactly
@@ -595,7 +604,7 @@ void b200lu_default_options(b200lu_options* opt) {
   opt->device = 0;
   opt->stream = nullptr;
   opt->refine_capacity = 20;  // include/rlu/refine.hpp:14
-  opt->reserved = 0;
+  opt->flags = 0;
 }
 
 const char* b200lu_status_string(b200lu_status s) {
@@ -637,6 +646,7 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   h->device = opt.device;
   h->pivot_floor = opt.pivot_floor;
   h->refine_capacity = opt.refine_capacity > 0 ? std::min(opt.refine_capacity, 64) : 20;
+  h->strict_order = (opt.flags & B200LU_FLAG_STRICT_ORDER) != 0;
   CU_TRY(h, cudaSetDevice(h->device));
   if (opt.stream) {
     h->stream = static_cast<cudaStream_t>(opt.stream);
@@ -645,7 +655,12 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
     h->owns_stream = true;
   }
 
-  const std::string err = build_schedule(*sym, kSmallSlot, h->sched);
+  // Sweep throttle (see schedule.hpp, fill_start_thresholds). Tunable for experiments; the
+  // defaults are what DESIGN.md reports.
+  if (const char* e = std::getenv("B200LU_SOLVE_LOOKAHEAD_LEVELS")) h->tune.solve_lookahead_levels = std::atoll(e);
+  if (const char* e = std::getenv("B200LU_SOLVE_MIN_WINDOW")) h->tune.solve_min_window = std::atoll(e);
+  if (const char* e = std::getenv("B200LU_SOLVE_MAX_WINDOW")) h->tune.solve_max_window = std::atoll(e);
+  const std::string err = build_schedule(*sym, h->tune, h->sched);
   if (!err.empty()) {
     h->last_error = err;
     return B200LU_INVALID_ARGUMENT;
@@ -671,6 +686,20 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   ST_TRY(dev_upload(h, &h->d_lower_order, S.lower_order));
   ST_TRY(dev_upload(h, &h->d_upper_order, S.upper_order));
   ST_TRY(dev_upload(h, &h->d_pair_row_ptr, S.pair_row_ptr));
+  ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
+  ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
+  {
+    auto factor_meta = [&S](const std::vector<int32_t>& rows) {
+      std::vector<FactorMeta> m(rows.size());
+      for (size_t r = 0; r < rows.size(); ++r) {
+        const int32_t i = rows[r];
+        m[r] = FactorMeta{i, S.row_ptr[i], S.diag[i], S.row_ptr[i + 1]};
+      }
+      return m;
+    };
+    ST_TRY(dev_upload(h, &h->d_small_meta, factor_meta(S.small_rows)));
+    ST_TRY(dev_upload(h, &h->d_big_meta, factor_meta(S.big_rows)));
+  }
 
   // scatter: inverse map (slot -> source entry), scale only on the matching path
   {
@@ -763,7 +792,7 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   int64_t max_big = 0;
   for (int32_t i : S.big_rows) max_big = std::max<int64_t>(max_big, S.row_ptr[i + 1] - S.row_ptr[i]);
   h->big_slot = static_cast<int>(std::min<int64_t>((max_big + 63) / 64 * 64, kMaxBigSlot));
-  h->factor_smem = (static_cast<size_t>(kFactorWarps) * kSmallSlot + h->big_slot) * sizeof(double);
+  h->factor_smem = (static_cast<size_t>(kFactorWarps) * h->tune.small_slot + h->big_slot) * sizeof(double);
   int occ = 0;
   if (h->dest16) {
     CU_TRY(h, cudaFuncSetAttribute(factor_kernel<uint16_t, kFactorWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -782,9 +811,12 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   }
   h->factor_grid = prop.multiProcessorCount * occ;
   int occ_tri = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri, lower_kernel, 128, 0));
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri, tri_kernel<false, false>, 256, 0));
   int occ_tri_u = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_u, upper_kernel, 128, 0));
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_u, tri_kernel<true, false>, 256, 0));
+  int occ_tri_d = 0;
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_d, tri_kernel<true, true>, 256, 0));
+  occ_tri_u = std::min(occ_tri_u, occ_tri_d);
   h->tri_grid = prop.multiProcessorCount * std::max(1, std::min(occ_tri, occ_tri_u));
   CU_TRY(h, cudaStreamSynchronize(h->stream));
   h->last_error.clear();
@@ -796,7 +828,8 @@ void b200lu_destroy(b200lu_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_small_rows, h->d_big_rows, h->d_lower_order,
-                  h->d_upper_order, h->d_pair_row_ptr, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p,
+                  h->d_upper_order, h->d_pair_row_ptr, h->d_lower_meta, h->d_upper_meta, h->d_small_meta,
+                  h->d_big_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p,
                   h->d_pq, h->d_row_scale, h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_a_vals, h->d_work,
                   h->d_values, h->d_w, h->d_t1, h->d_t2, h->d_in, h->d_in2, h->d_out, h->d_counters, h->d_failed,
                   h->d_scal, h->d_partials, h->d_ticket, h->d_V, h->d_Z, h->d_wv, h->d_r, h->d_cand, h->d_best,
@@ -1014,7 +1047,7 @@ b200lu_status b200lu_schedule_probe(const b200lu_symbolic_view* sym, b200lu_stat
                                     char* error_buf, int error_buf_len) {
   if (!sym) return B200LU_INVALID_ARGUMENT;
   Schedule S;
-  const std::string err = build_schedule(*sym, kSmallSlot, S);
+  const std::string err = build_schedule(*sym, ScheduleTuning{}, S);
   if (error_buf && error_buf_len > 0) {
     std::strncpy(error_buf, err.c_str(), static_cast<size_t>(error_buf_len) - 1);
     error_buf[error_buf_len - 1] = '\0';

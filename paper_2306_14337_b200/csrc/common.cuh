@@ -36,14 +36,38 @@ __device__ __forceinline__ void publish(double* p, double v) {
   st_l2(p, v);
 }
 
-// Spins until *p has been published by its owner.
+// Spins until *p has been published by its owner (no back-off: callers only spin on values
+// whose producer is running or about to).
 __device__ __forceinline__ double wait_value(const double* p) {
   double v = ld_l2(p);
-  while (is_pending(v)) {
-    __nanosleep(32);
-    v = ld_l2(p);
-  }
+  while (is_pending(v)) v = ld_l2(p);
   return v;
+}
+
+__device__ __forceinline__ int32_t ld_l2_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
+// Throttle of a sync-free sweep: a claimed row sleeps until `start` rows of the sweep have
+// finished (schedule.hpp, fill_start_thresholds). One lane polls one counter, with a sleep
+// proportional to how far away the row still is.
+__device__ __forceinline__ void wait_for_start(const int32_t* finished, int32_t start, int lane) {
+  if (start > 0) {
+    if (lane == 0) {
+      int32_t c = ld_l2_s32(finished);
+      while (c < start) {
+        __nanosleep(min(4000, max(64, (start - c) * 4)));
+        c = ld_l2_s32(finished);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // a - b*c with two roundings (the reference's x86-64 baseline build has no FMA

@@ -80,21 +80,28 @@ build_dest_kernel(int32_t n, const int32_t* __restrict__ row_ptr, const int32_t*
 // in ascending order, so every slot receives its updates in the reference's order and the
 // result is bit-identical to the sequential CPU run regardless of scheduling. What changes:
 //   * rows are claimed in dependency-level order from two queues (rows a warp slot can hold,
-//     and wide rows that use the CTA's wide slot), by persistent warps;
+//     and wide rows that use the CTA's wide slot) by persistent warps, so a row starts long
+//     before its last dependency finishes and consumes its already-final pivots ahead of time;
 //   * row i is staged in shared memory while its pivots are applied;
-//   * there are no ready flags: a finished row publishes its values into `values`, which K1
-//     armed with the pending marker; a consumer lane that needs u_dj simply waits on that
-//     8-byte value (Ginkgo's sentinel idea, applied to the factorization);
-//   * the column->slot lookup is the precomputed destination table.
+//   * there are no ready flags: a finished row publishes its diagonal and upper entries into
+//     `values`, which K1 armed with the pending marker; a consumer simply waits on the 8-byte
+//     values it needs (Ginkgo's sentinel idea, applied to the factorization);
+//   * the column->slot lookup is the precomputed destination table, streamed once;
+//   * the loads of kPivotGroup consecutive pivots (diagonal, upper entries, destinations) are
+//     issued together before the first of them is consumed, so a row with hundreds of
+//     finished pivots is bound by throughput, not by one memory round trip per pivot.
+struct FactorMeta {
+  int32_t row, lo, dg, hi;
+};
+
 struct FactorArgs {
-  int32_t n;
   int32_t n_small, n_big;
   int32_t small_slot, big_slot;  // capacities in doubles
   const int32_t* row_ptr;
   const int32_t* col;
   const int32_t* diag;
-  const int32_t* small_rows;
-  const int32_t* big_rows;
+  const FactorMeta* small_meta;  // per claim position of the two queues
+  const FactorMeta* big_meta;
   const int64_t* pair_row_ptr;
   const void* dest;
   double* work;     // scattered input values (K1), also the in-place fallback for over-wide rows
@@ -104,9 +111,12 @@ struct FactorArgs {
   int32_t* failed_row;  // atomicMin target, initialised to INT32_MAX
 };
 
+constexpr int kPivotGroup = 4;
+
 template <typename DestT>
-__device__ __forceinline__ void factor_row(const FactorArgs& a, int32_t i, double* row, int lane) {
-  const int32_t lo = a.row_ptr[i], dg = a.diag[i], hi = a.row_ptr[i + 1];
+__device__ __forceinline__ void factor_row(const FactorArgs& a, const FactorMeta mt, double* row, int lane) {
+  const unsigned full = 0xffffffffu;
+  const int32_t i = mt.row, lo = mt.lo, dg = mt.dg, hi = mt.hi;
   const int32_t len = hi - lo, nl = dg - lo;
   const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
   const double* values = a.values;
@@ -116,7 +126,7 @@ __device__ __forceinline__ void factor_row(const FactorArgs& a, int32_t i, doubl
   }
   __syncwarp();
 
-  int64_t p = a.pair_row_ptr[i];
+  int64_t p = nl > 0 ? a.pair_row_ptr[i] : 0;
   for (int32_t k0 = 0; k0 < nl; k0 += 32) {
     // Lane q of this chunk resolves the metadata of pivot k0+q; the walk below is sequential.
     int32_t my_dd = 0, my_m = 0;
@@ -126,41 +136,56 @@ __device__ __forceinline__ void factor_row(const FactorArgs& a, int32_t i, doubl
       my_m = __ldg(a.row_ptr + d + 1) - my_dd - 1;
     }
     const int32_t cnt = min(32, nl - k0);
-    for (int32_t q = 0; q < cnt; ++q) {
-      const int32_t dd = __shfl_sync(0xffffffffu, my_dd, q);
-      const int32_t m = __shfl_sync(0xffffffffu, my_m, q);
-      // Issue this lane's loads before waiting on anything.
-      double u0 = 0.0, u1 = 0.0;
-      int32_t s0 = 0, s1 = 0;
-      const bool h0 = lane < m, h1 = lane + 32 < m;
-      if (h0) { u0 = ld_l2(values + dd + 1 + lane); s0 = dest[p + lane]; }
-      if (h1) { u1 = ld_l2(values + dd + 33 + lane); s1 = dest[p + 32 + lane]; }
-      const double udiag = wait_value(values + dd);
-      const double alpha = row[k0 + q] / udiag;  // src/numeric.cpp:40
-      if (h0) {
-        while (is_pending(u0)) { __nanosleep(32); u0 = ld_l2(values + dd + 1 + lane); }
-        row[s0] = sub_prod(row[s0], alpha, u0);  // src/numeric.cpp:44
+    for (int32_t q0 = 0; q0 < cnt; q0 += kPivotGroup) {
+      int32_t dd[kPivotGroup], m[kPivotGroup], s0[kPivotGroup], s1[kPivotGroup];
+      int64_t pg[kPivotGroup];
+      double ud[kPivotGroup], u0[kPivotGroup], u1[kPivotGroup];
+#pragma unroll
+      for (int g = 0; g < kPivotGroup; ++g) {
+        const int32_t q = q0 + g;
+        dd[g] = __shfl_sync(full, my_dd, q & 31);
+        m[g] = __shfl_sync(full, my_m, q & 31);
+        if (q >= cnt) m[g] = -1;  // no such pivot
+        pg[g] = p;
+        p += max(m[g], 0);
+        ud[g] = 1.0; u0[g] = 0.0; u1[g] = 0.0; s0[g] = 0; s1[g] = 0;
+        if (m[g] >= 0) ud[g] = ld_l2(values + dd[g]);
+        if (lane < m[g]) { u0[g] = ld_l2(values + dd[g] + 1 + lane); s0[g] = dest[pg[g] + lane]; }
+        if (lane + 32 < m[g]) { u1[g] = ld_l2(values + dd[g] + 33 + lane); s1[g] = dest[pg[g] + 32 + lane]; }
       }
-      if (h1) {
-        while (is_pending(u1)) { __nanosleep(32); u1 = ld_l2(values + dd + 33 + lane); }
-        row[s1] = sub_prod(row[s1], alpha, u1);
+#pragma unroll
+      for (int g = 0; g < kPivotGroup; ++g) {
+        if (m[g] < 0) break;  // warp-uniform
+        const bool h0 = lane < m[g], h1 = lane + 32 < m[g];
+        // One combined wait: whatever is still pending is re-read until the producer's
+        // publication (diagonal and upper entries of row d) has landed.
+        while (__any_sync(full, is_pending(ud[g]) || is_pending(u0[g]) || is_pending(u1[g]))) {
+          if (is_pending(ud[g])) ud[g] = ld_l2(values + dd[g]);
+          if (is_pending(u0[g])) u0[g] = ld_l2(values + dd[g] + 1 + lane);
+          if (is_pending(u1[g])) u1[g] = ld_l2(values + dd[g] + 33 + lane);
+        }
+        const int32_t k = k0 + q0 + g;
+        const double alpha = row[k] / ud[g];  // src/numeric.cpp:40
+        if (h0) row[s0[g]] = sub_prod(row[s0[g]], alpha, u0[g]);  // src/numeric.cpp:44
+        if (h1) row[s1[g]] = sub_prod(row[s1[g]], alpha, u1[g]);
+        for (int32_t c = lane + 64; c < m[g]; c += 32) {
+          const double u = wait_value(values + dd[g] + 1 + c);
+          const int32_t s = dest[pg[g] + c];
+          row[s] = sub_prod(row[s], alpha, u);
+        }
+        // l_id is final (src/numeric.cpp:41); nothing waits on strict-lower entries during the
+        // factorization, so a plain store is enough.
+        if (lane == 0) a.values[lo + k] = alpha;
+        __syncwarp();
       }
-      for (int32_t c = lane + 64; c < m; c += 32) {
-        const double u = wait_value(values + dd + 1 + c);
-        const int32_t s = dest[p + c];
-        row[s] = sub_prod(row[s], alpha, u);
-      }
-      p += m;
-      __syncwarp();
-      if (lane == 0) row[k0 + q] = alpha;  // src/numeric.cpp:41
     }
-    __syncwarp();
   }
 
   // src/numeric.cpp:48: the row completes (and is published) even when its pivot fails, so
   // dependents never hang (include/rlu/schedule.hpp:29-33); the lowest failing row wins (82-87).
+  // Publish what other rows wait on first: the diagonal and the upper entries.
+  for (int32_t c = nl + lane; c < len; c += 32) publish(a.values + lo + c, row[c]);
   if (lane == 0 && fabs(row[nl]) <= a.pivot_floor) atomicMin(a.failed_row, i);
-  for (int32_t c = lane; c < len; c += 32) publish(a.values + lo + c, row[c]);
 }
 
 template <typename DestT, int WARPS>
@@ -179,10 +204,10 @@ factor_kernel(const FactorArgs a) {
       if (lane == 0) r = atomicAdd(a.counters + 1, 1);
       r = __shfl_sync(0xffffffffu, r, 0);
       if (r >= a.n_big) break;
-      const int32_t i = a.big_rows[r];
-      const int32_t len = a.row_ptr[i + 1] - a.row_ptr[i];
-      double* row = len <= a.big_slot ? big_slot : a.work + a.row_ptr[i];
-      factor_row<DestT>(a, i, row, lane);
+      const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.big_meta) + r);
+      const FactorMeta mt{m4.x, m4.y, m4.z, m4.w};
+      double* row = (mt.hi - mt.lo) <= a.big_slot ? big_slot : a.work + mt.lo;
+      factor_row<DestT>(a, mt, row, lane);
       __syncwarp();
     }
   }
@@ -191,7 +216,8 @@ factor_kernel(const FactorArgs a) {
     if (lane == 0) r = atomicAdd(a.counters, 1);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= a.n_small) break;
-    factor_row<DestT>(a, a.small_rows[r], small_slot, lane);
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.small_meta) + r);
+    factor_row<DestT>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, small_slot, lane);
     __syncwarp();
   }
 }

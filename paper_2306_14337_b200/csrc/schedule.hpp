@@ -16,6 +16,15 @@
 
 namespace b200lu {
 
+// One record per claim position, so a worker learns everything about its row from one 16-byte
+// load instead of a chain of dependent index loads.
+struct RowMeta {
+  int32_t row;    // row index in the permuted matrix
+  int32_t beg;    // first entry the worker touches
+  int32_t end;    // one past the last entry
+  int32_t start;  // the row may start once this many rows of the sweep have finished
+};
+
 struct Schedule {
   int64_t n = 0, nnz = 0, nnz_lower = 0, update_pairs = 0;
   int64_t lower_levels = 0, upper_levels = 0, max_row_len = 0;
@@ -23,12 +32,45 @@ struct Schedule {
   // Rows by ascending L-level (ties by index), split by row length into the rows a single warp
   // slot holds and the wide rows that need the per-CTA wide slot.
   std::vector<int32_t> small_rows, big_rows;
-  std::vector<int32_t> lower_order;  // all rows, L-level order (triangular solve with L)
-  std::vector<int32_t> upper_order;  // all rows, U-level order (triangular solve with U)
+  std::vector<int32_t> lower_order;  // all rows, L-level order
+  std::vector<int32_t> upper_order;  // all rows, U-level order
   std::vector<int64_t> pair_row_ptr;  // n+1: first update pair of each row
+  std::vector<int32_t> lower_level, upper_level;  // per row
+  std::vector<int32_t> lower_width, upper_width;  // rows per level
+  std::vector<RowMeta> lower_meta, upper_meta;    // triangular sweeps, per claim position
 };
 
-inline std::string build_schedule(const b200lu_symbolic_view& s, int64_t small_slot, Schedule& out) {
+// Start thresholds of a triangular sweep. Row at claim position r may begin once `start`
+// rows have finished, chosen so that it is at most `lookahead_levels` dependency levels (and
+// between `min_window` and `max_window` rows) ahead of the completed frontier: close enough
+// that the values it then spins on are about to be produced, far enough that it has consumed
+// its long-finished entries before its last dependency arrives. The threshold is a throttle
+// on L2 polling only — ordering is enforced by the values themselves — and start <= r keeps it
+// deadlock-free: the lowest unfinished row in claim order always finds its threshold met.
+inline void fill_start_thresholds(std::vector<RowMeta>& meta, const std::vector<int32_t>& level,
+                                  const std::vector<int32_t>& width, int64_t lookahead_levels,
+                                  int64_t min_window, int64_t max_window) {
+  const int64_t n = static_cast<int64_t>(meta.size());
+  const int64_t levels = static_cast<int64_t>(width.size());
+  std::vector<int64_t> level_begin(static_cast<size_t>(levels) + 1, 0);  // rows in levels < l
+  for (int64_t l = 0; l < levels; ++l) level_begin[l + 1] = level_begin[l] + width[l];
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t l = level[meta[r].row];
+    const int64_t by_level = level_begin[std::max<int64_t>(0, l - lookahead_levels)];
+    int64_t start = std::max(by_level, r - max_window);
+    start = std::min(start, r - min_window);
+    meta[r].start = static_cast<int32_t>(std::max<int64_t>(0, start));
+  }
+}
+
+struct ScheduleTuning {
+  int64_t small_slot = 512;
+  int64_t solve_lookahead_levels = 48;
+  int64_t solve_min_window = 64;
+  int64_t solve_max_window = 1 << 20;
+};
+
+inline std::string build_schedule(const b200lu_symbolic_view& s, const ScheduleTuning& tune, Schedule& out) {
   const int64_t n = s.n;
   const int64_t nnz = s.nnz_factors;
   if (n < 0 || nnz < 0) return "negative dimensions";
@@ -100,12 +142,33 @@ inline std::string build_schedule(const b200lu_symbolic_view& s, int64_t small_s
   out.lower_order = level_sort(llev, lmax + 1, false);
   out.upper_order = level_sort(ulev, umax + 1, true);
 
+  out.lower_level = llev;
+  out.upper_level = ulev;
+  out.lower_width.assign(static_cast<size_t>(lmax + 1), 0);
+  out.upper_width.assign(static_cast<size_t>(umax + 1), 0);
+  for (int64_t i = 0; i < n; ++i) {
+    ++out.lower_width[llev[i]];
+    ++out.upper_width[ulev[i]];
+  }
+
+  out.lower_meta.resize(n);
+  out.upper_meta.resize(n);
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t il = out.lower_order[r], iu = out.upper_order[r];
+    out.lower_meta[r] = RowMeta{il, out.row_ptr[il], out.diag[il], 0};          // strict-lower entries
+    out.upper_meta[r] = RowMeta{iu, out.diag[iu] + 1, out.row_ptr[iu + 1], 0};  // strict-upper entries
+  }
+  fill_start_thresholds(out.lower_meta, llev, out.lower_width, tune.solve_lookahead_levels,
+                        tune.solve_min_window, tune.solve_max_window);
+  fill_start_thresholds(out.upper_meta, ulev, out.upper_width, tune.solve_lookahead_levels,
+                        tune.solve_min_window, tune.solve_max_window);
+
   out.small_rows.clear();
   out.big_rows.clear();
   for (int64_t r = 0; r < n; ++r) {
     const int32_t i = out.lower_order[r];
     const int64_t len = s.row_offsets[i + 1] - s.row_offsets[i];
-    (len <= small_slot ? out.small_rows : out.big_rows).push_back(i);
+    (len <= tune.small_slot ? out.small_rows : out.big_rows).push_back(i);
   }
   return "";
 }

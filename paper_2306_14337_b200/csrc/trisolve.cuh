@@ -2,6 +2,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "schedule.hpp"
 
 namespace b200lu {
 
@@ -42,69 +43,101 @@ fill_pending_kernel(int64_t n, double* __restrict__ x) {
 
 struct TriArgs {
   int32_t n;
-  const int32_t* row_ptr;
+  const RowMeta* meta;    // per claim position, dependency-level order
   const int32_t* col;
   const int32_t* diag;
-  const int32_t* order;   // rows in dependency-level order
   const double* values;
   const double* y;
   double* x;              // armed with the pending marker; each row publishes x[i]
-  int32_t* counter;       // ticket
+  int32_t* counter;       // claim ticket
+  int32_t* finished;      // rows finished so far in this sweep
   int32_t* failed_row;    // upper only: atomicMax target, initialised to -1
 };
 
-// Reference: lower_core, src/trisolve.cpp:28-42 — x_i = y_i - sum_{d<i} l_id x_d over the
-// strict-lower entries in ascending column order (kept: one thread accumulates one row, so x
-// is bit-identical to the CPU result). Rows are claimed 32 at a time in level order; a thread
-// that needs x_d waits on the value itself (Ginkgo's NaN-sentinel scheme).
-__global__ void __launch_bounds__(128)
-lower_kernel(const TriArgs a) {
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    int32_t r0 = 0;
-    if (lane == 0) r0 = atomicAdd(a.counter, 32);
-    r0 = __shfl_sync(0xffffffffu, r0, 0);
-    if (r0 >= a.n) break;
-    const int32_t r = r0 + lane;
-    if (r < a.n) {
-      const int32_t i = a.order[r];
-      const int32_t lo = a.row_ptr[i], dg = a.diag[i];
-      double acc = a.y[i];
-      for (int32_t k = lo; k < dg; ++k) {
-        const double xd = wait_value(a.x + a.col[k]);
-        acc = sub_prod(acc, a.values[k], xd);  // src/trisolve.cpp:38
-      }
-      publish(a.x + i, acc);
-    }
-    __syncwarp();
-  }
-}
-
-// Reference: upper_core, src/trisolve.cpp:46-68 — x_i = (y_i - sum_{j>i} u_ij x_j) / u_ii.
-// An exactly zero diagonal is recorded (the highest such row is what the reference's
+// Reference: lower_core (src/trisolve.cpp:28-42): x_i = y_i - sum_{d<i} l_id x_d, and
+// upper_core (46-68): x_i = (y_i - sum_{j>i} u_ij x_j) / u_ii, rows in descending order.
+//
+// One warp owns one row, claimed in dependency-level order. The 32 lanes fetch 32 entries at a
+// time (coalesced value/column loads, a gather of x; the next chunk is in flight while the
+// current one is folded) and each lane waits on the x it needs — the value itself is the ready
+// flag (Ginkgo's NaN-sentinel scheme). The products are folded into the
+// accumulator ONE AT A TIME, consuming every already-available leading entry while later ones
+// are still in flight, so when the last dependency lands only its own term is left to add.
+//
+// Fold order. kDescending == false walks the entries in ascending column order, the
+// reference's summation order (src/trisolve.cpp:38,57): x is then bit-identical to the CPU
+// result. For L that is also the order in which the dependencies are produced. For U the
+// dependencies are produced in DESCENDING column order (row i+1 finishes last and is the first
+// entry of row i), so the ascending fold leaves the whole row on the critical path behind its
+// last arrival; kDescending == true folds U rows from the last column to the first instead:
+// same terms, fixed (deterministic) order, different rounding of the partial sums.
+//
+// An exactly zero U diagonal is recorded (the highest such row is what the reference's
 // lowest-virtual-index rule reports, src/trisolve.cpp:60-66) and the row still completes.
-__global__ void __launch_bounds__(128)
-upper_kernel(const TriArgs a) {
+template <bool kUpper, bool kDescending>
+__global__ void __launch_bounds__(256)
+tri_kernel(const TriArgs a) {
   const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   while (true) {
-    int32_t r0 = 0;
-    if (lane == 0) r0 = atomicAdd(a.counter, 32);
-    r0 = __shfl_sync(0xffffffffu, r0, 0);
-    if (r0 >= a.n) break;
-    const int32_t r = r0 + lane;
-    if (r < a.n) {
-      const int32_t i = a.order[r];
-      const int32_t dg = a.diag[i], hi = a.row_ptr[i + 1];
-      double acc = a.y[i];
-      for (int32_t k = dg + 1; k < hi; ++k) {
-        const double xj = wait_value(a.x + a.col[k]);
-        acc = sub_prod(acc, a.values[k], xj);  // src/trisolve.cpp:57
-      }
-      const double d = a.values[dg];
-      if (d == 0.0) atomicMax(a.failed_row, i);
-      publish(a.x + i, acc / d);
+    int32_t r = 0;
+    if (lane == 0) r = atomicAdd(a.counter, 1);
+    r = __shfl_sync(full, r, 0);
+    if (r >= a.n) break;
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
+    const int32_t i = m4.x, beg = m4.y, end = m4.z;
+    double acc = a.y[i];
+    double dval = 1.0;
+    if (kUpper) dval = a.values[beg - 1];  // u_ii sits right before the strict-upper entries
+    wait_for_start(a.finished, m4.w, lane);
+
+    // entry handled by this lane in chunk c (chunks and lanes walk the row in fold order)
+    auto entry = [&](int32_t c) { return kDescending ? end - 1 - (c * 32 + lane) : beg + c * 32 + lane; };
+    const int32_t nent = end - beg;
+    const int32_t nchunks = (nent + 31) >> 5;
+    const double* xp = a.x;
+    double v = 0.0, xv = 0.0;
+    if (lane < nent) {
+      const int32_t k = entry(0);
+      v = a.values[k];
+      xp = a.x + __ldg(a.col + k);
+      xv = ld_l2(xp);
     }
-    __syncwarp();
+    for (int32_t c = 0; c < nchunks; ++c) {
+      // software pipeline: issue the next chunk's loads before folding this one
+      const double* xp_next = a.x;
+      double v_next = 0.0, xv_next = 0.0;
+      if ((c + 1) * 32 + lane < nent) {
+        const int32_t k = entry(c + 1);
+        v_next = a.values[k];
+        xp_next = a.x + __ldg(a.col + k);
+        xv_next = ld_l2(xp_next);
+      }
+      const int32_t cnt = min(32, nent - c * 32);
+      int32_t q = 0;
+      while (q < cnt) {
+        const unsigned ready = __ballot_sync(full, !is_pending(xv));
+        const unsigned from_q = ~(ready >> q);  // bit t set <=> entry q+t is still pending
+        int32_t run = from_q == 0u ? 32 : __ffs(static_cast<int>(from_q)) - 1;
+        run = min(run, cnt - q);
+        const double prod = __dmul_rn(v, xv);
+#pragma unroll 8
+        for (int32_t t = 0; t < run; ++t) acc = __dsub_rn(acc, __shfl_sync(full, prod, q + t));
+        q += run;
+        if (q < cnt && is_pending(xv)) xv = ld_l2(xp);
+      }
+      v = v_next;
+      xp = xp_next;
+      xv = xv_next;
+    }
+    if (kUpper) {
+      if (lane == 0 && dval == 0.0) atomicMax(a.failed_row, i);
+      acc = acc / dval;
+    }
+    if (lane == 0) {
+      publish(a.x + i, acc);
+      red_add_s32(a.finished, 1);
+    }
   }
 }
 

@@ -111,6 +111,7 @@ class FactorOptions:
     device: int = 0
     stream: int | None = None      # raw cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
     refine_capacity: int = 20
+    strict_order: bool = False     # U sweep in the reference's summation order (bit-identical x)
 
 
 @dataclass
@@ -157,6 +158,7 @@ class NumericFactors:
         o.device = self.options.device
         o.stream = self.options.stream
         o.refine_capacity = self.options.refine_capacity
+        o.flags = _capi.FLAG_STRICT_ORDER if self.options.strict_order else 0
         st = L.b200lu_create(C.byref(v), C.byref(o), C.byref(self._h))
         if st != _capi.OK:
             msg = L.b200lu_last_error(self._h).decode() if self._h else ""
@@ -269,7 +271,15 @@ def _values_ptr(A: CsrMatrix):
 
 
 def _guard_pattern(f: NumericFactors, A: CsrMatrix):
-    """scatter_values' guards, src/numeric.cpp:15-18."""
+    """scatter_values' guards, src/numeric.cpp:15-18. The element-wise pattern comparison
+    (pattern_equal) is done once per (matrix object, handle): a CsrMatrix whose pattern arrays
+    were verified against this handle is trusted afterwards, so a sequence that re-submits the
+    same pattern arrays with new values pays the 8*(n+1+nnz)-byte comparison only once."""
+    if not A.has_values():
+        if getattr(A, "_verified_for", None) == id(f):
+            raise Error("scatter_values: matrix has no values")
+    if getattr(A, "_verified_for", None) == id(f) and A.has_values():
+        return
     ro, ci = _i64(A.row_offsets), _i64(A.col_indices)
     st = _capi.PATTERN_MISMATCH
     if A.nrows == A.ncols and ro.size == A.nrows + 1 and ci.size == len(f.symbolic.src_col_indices):
@@ -278,6 +288,10 @@ def _guard_pattern(f: NumericFactors, A: CsrMatrix):
         raise PatternMismatchError("matrix pattern differs from the analyzed pattern")
     if not A.has_values():
         raise Error("scatter_values: matrix has no values")
+    try:
+        A._verified_for = id(f)
+    except Exception:
+        pass
 
 
 def reset_values(f: NumericFactors, A: CsrMatrix):

@@ -14,6 +14,10 @@ from oracle import refbridge as rb
 from tests.fixtures import csr_fixture, dense_fixture, golden_fixture, kkt_fixture
 
 pytestmark = pytest.mark.gpu
+# The U sweep's summation order is selectable (include/b200lu.h, B200LU_FLAG_STRICT_ORDER): bitwise
+# comparisons of upper_solve / solve_system use the reference's order; the default (device
+# production order) is covered by test_default_u_sweep_order_* on the residual.
+STRICT = rlu.FactorOptions(strict_order=True)
 needs_ref = pytest.mark.skipif(not rb.available(), reason="oracle/_ref/librlu_ref.so not built")
 
 
@@ -50,7 +54,7 @@ def test_committed_fixtures_bitwise(name):
     """Inputs + the reference's outputs from tests/golden (no reference needed at run time)."""
     fx = golden_fixture(name)
     g = fx.golden
-    f = rlu.NumericFactors(fx.sym)
+    f = rlu.NumericFactors(fx.sym, STRICT)
     for k in range(len(fx.values)):
         rlu.reset_values(f, fx.matrix(k))
         assert not f.valid
@@ -217,7 +221,7 @@ def test_trisolve_bitwise_and_composition(scaling):
         n = rng.uniform_int(10, 200)
         A = rng.random_sparse(n, 5, 0.1, 1.0, True)
         fx = csr_fixture(A, scaling, True)
-        f = rlu.factorize(fx.sym, fx.matrix())
+        f = rlu.factorize(fx.sym, fx.matrix(), STRICT)
         lu = f.values
         b = rng.random_vector(n)
         lo = rlu.lower_solve(f, b)
@@ -267,6 +271,29 @@ def test_no_device_allocation_after_create():
     rlu.refactorize(f, fx.matrix())
     rlu.fgmres_refine(f, b, x0)
     assert f.stats["alloc_events"] == before
+
+
+@needs_ref
+@pytest.mark.parametrize("scaling", [False, True])
+def test_default_u_sweep_order_is_deterministic_and_as_accurate(scaling):
+    """Default options fold U rows in device production order: same terms, different rounding.
+    Tolerance: the direct residual may not exceed the reference-order residual by more than 4x
+    (+1e-15 absolute), and two runs must agree bit for bit."""
+    fx = kkt_fixture(6300, 2700, use_scaling=scaling)
+    f, fs = rlu.NumericFactors(fx.sym), rlu.NumericFactors(fx.sym, STRICT)
+    for k in (0, len(fx.values) - 1):
+        rlu.refactorize(f, fx.matrix(k))
+        rlu.refactorize(fs, fx.matrix(k))
+        assert np.array_equal(f.values, fs.values)
+        b = fx.rhs[k]
+        assert np.array_equal(rlu.lower_solve(f, b), rlu.lower_solve(fs, b))  # L sweep: always exact
+        x, xs = rlu.solve_system(f, b), rlu.solve_system(fs, b)
+        assert np.array_equal(x, rlu.solve_system(f, b))
+        assert np.array_equal(xs, fx.oracle.solve_system(fs.values, b)[0])
+        r, rs = _relres(fx, x, b, k), _relres(fx, xs, b, k)
+        assert r <= 4 * rs + 1e-15, (r, rs)
+        out = rlu.fgmres_refine(f, b, x)
+        assert _relres(fx, out.x, b, k) <= 1e-14
 
 
 # --------------------------------------------------------------- SpMV / BLAS
@@ -408,7 +435,7 @@ def test_kkt_sequence_c1_analyze_once_refactorize_rest(scaling):
     """BASELINE config C1 (ACTIVSg200-shaped, n+m = 9000): one analysis, 10 refactor/solve;
     acceptance.cpp:236-272 (relres <= 1e-8 on every system, median refinement iterations <= 2)."""
     fx = kkt_fixture(6300, 2700, use_scaling=scaling)
-    f = rlu.NumericFactors(fx.sym)
+    f = rlu.NumericFactors(fx.sym, STRICT)
     ref_num = rb.RefNumeric(fx.ref_sym)
     iters = []
     for k in range(len(fx.values)):
