@@ -159,10 +159,16 @@ __device__ __forceinline__ void factor_row(const FactorArgs& a, const FactorMeta
         const bool h0 = lane < m[g], h1 = lane + 32 < m[g];
         // One combined wait: whatever is still pending is re-read until the producer's
         // publication (diagonal and upper entries of row d) has landed.
+        // While waiting, the still-pending values of the LATER pivots of the group are re-read
+        // too (their loads overlap this wait), so a run of just-finished pivots costs one round
+        // trip instead of one per pivot.
         while (__any_sync(full, is_pending(ud[g]) || is_pending(u0[g]) || is_pending(u1[g]))) {
-          if (is_pending(ud[g])) ud[g] = ld_l2(values + dd[g]);
-          if (is_pending(u0[g])) u0[g] = ld_l2(values + dd[g] + 1 + lane);
-          if (is_pending(u1[g])) u1[g] = ld_l2(values + dd[g] + 33 + lane);
+#pragma unroll
+          for (int e = g; e < kPivotGroup; ++e) {
+            if (is_pending(ud[e])) ud[e] = ld_l2(values + dd[e]);
+            if (is_pending(u0[e])) u0[e] = ld_l2(values + dd[e] + 1 + lane);
+            if (is_pending(u1[e])) u1[e] = ld_l2(values + dd[e] + 33 + lane);
+          }
         }
         const int32_t k = k0 + q0 + g;
         const double alpha = row[k] / ud[g];  // src/numeric.cpp:40
