@@ -152,12 +152,14 @@ inline void reset_values(NumericFactors& f, const CsrMatrix& A) {  // src/numeri
 }
 inline void factorize_scattered(NumericFactors& f) {  // src/numeric.cpp:79
   std::int64_t row = -1;
-  f.check(b200lu_factorize_scattered(f.handle(), &row), row);
+  const b200lu_status st = b200lu_factorize_scattered(f.handle(), &row);  // call first: `row` is an output
+  f.check(st, row);
 }
 inline void refactorize(NumericFactors& f, const CsrMatrix& A) {  // src/numeric.cpp:70-73
   detail::guard(f, A);
   std::int64_t row = -1;
-  f.check(b200lu_refactorize(f.handle(), A.values.data(), 0, &row), row);
+  const b200lu_status st = b200lu_refactorize(f.handle(), A.values.data(), 0, &row);
+  f.check(st, row);
 }
 inline NumericFactors factorize(const SymbolicView& sym, const CsrMatrix& A, const FactorOptions& opt = {}) {
   NumericFactors f(sym, opt);  // src/numeric.cpp:62-68
@@ -173,13 +175,16 @@ inline DenseVector lower_solve(const NumericFactors& f, const DenseVector& y) { 
 inline DenseVector upper_solve(const NumericFactors& f, const DenseVector& y) {  // src/trisolve.cpp:81-88
   DenseVector x(y.size());
   std::int64_t row = -1;
-  f.check(b200lu_upper_solve(f.handle(), static_cast<index_t>(y.size()), y.data(), x.data(), 0, &row), row);
+  const b200lu_status st =
+      b200lu_upper_solve(f.handle(), static_cast<index_t>(y.size()), y.data(), x.data(), 0, &row);
+  f.check(st, row);
   return x;
 }
 inline void solve_system(const NumericFactors& f, const DenseVector& b, DenseVector& x) {  // src/trisolve.cpp:90-119
   if (x.size() != b.size()) x.resize(b.size());
   std::int64_t row = -1;
-  f.check(b200lu_solve(f.handle(), static_cast<index_t>(b.size()), b.data(), x.data(), 0, &row), row);
+  const b200lu_status st = b200lu_solve(f.handle(), static_cast<index_t>(b.size()), b.data(), x.data(), 0, &row);
+  f.check(st, row);
 }
 inline DenseVector solve_system(const NumericFactors& f, const DenseVector& b) {
   DenseVector x;
