@@ -76,12 +76,15 @@ typedef struct {
   int flags;           /* B200LU_FLAG_* */
 } b200lu_options;
 
-/* Summation order of the U sweep (upper_core, src/trisolve.cpp:52-58). The L/U values, the L
- * sweep and SpMV always reproduce the reference bit for bit. By default the U sweep folds each
- * row from its last column to its first — the order in which its dependencies are produced on
- * the device — which is deterministic but rounds the partial sums differently from the
- * reference. With this flag it folds in the reference's ascending column order and
- * upper_solve / solve_system are bit-identical to the CPU result, at a longer critical path. */
+/* Summation order of the triangular sweeps (lower_core / upper_core, src/trisolve.cpp:28-68).
+ * The L/U values and SpMV always reproduce the reference bit for bit. By default the sweeps sum
+ * each row's terms in an order chosen for the device: U rows are folded from the last column to
+ * the first (the order in which their dependencies are produced), and the narrow end of the
+ * dependency DAG runs inside one CTA with per-lane partial sums and a shuffle tree. That order is
+ * fixed — results are deterministic — but it rounds differently from the reference's serial sum.
+ * With this flag both sweeps run entirely in the sync-free kernel and fold in the reference's
+ * ascending column order: lower_solve / upper_solve / solve_system are then bit-identical to the
+ * CPU result, at a longer critical path. */
 #define B200LU_FLAG_STRICT_ORDER 1
 
 /* rlu::RefineConfig (include/rlu/refine.hpp:13-17) */
@@ -109,6 +112,10 @@ typedef struct {
   int64_t big_rows;         /* rows handled by the per-CTA wide slot */
   int64_t device_bytes;     /* total device memory owned by the handle */
   int64_t alloc_events;     /* device allocations performed so far (constant after create) */
+  int64_t lower_tail_rows;  /* rows / levels of the L sweep handled inside one CTA (0: no split) */
+  int64_t lower_tail_levels;
+  int64_t upper_tail_rows;  /* same for the U sweep */
+  int64_t upper_tail_levels;
 } b200lu_stats;
 
 void b200lu_default_options(b200lu_options* opt);
@@ -208,7 +215,8 @@ enum {
   B200LU_PHASE_PERMUTE = 4, /* solve_system prologue / epilogue */
   B200LU_PHASE_SPMV = 5,    /* K4: SpMV / fused residual */
   B200LU_PHASE_VECTOR = 6,  /* K4: dot, projection, axpy, scale */
-  B200LU_NUM_PHASES = 7
+  B200LU_PHASE_TAIL = 7,    /* K3: the narrow end of either sweep inside one cluster (default mode) */
+  B200LU_NUM_PHASES = 8
 };
 b200lu_status b200lu_set_timing(b200lu_handle* h, int enabled);
 b200lu_status b200lu_get_phase_times(b200lu_handle* h, double* ms_out, int64_t* count_out, int reset);

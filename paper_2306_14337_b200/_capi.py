@@ -40,7 +40,8 @@ class RefineOutcome(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(k, i64) for k in ("n", "nnz_factors", "nnz_source", "nnz_lower", "update_pairs",
                                    "lower_levels", "upper_levels", "max_row_len", "big_rows",
-                                   "device_bytes", "alloc_events")]
+                                   "device_bytes", "alloc_events", "lower_tail_rows",
+                                   "lower_tail_levels", "upper_tail_rows", "upper_tail_levels")]
 
 
 EXPORTS = {
@@ -78,7 +79,7 @@ EXPORTS = {
 }
 
 FLAG_STRICT_ORDER = 1
-PHASES = ("scatter", "factor", "lower", "upper", "permute", "spmv", "vector")
+PHASES = ("scatter", "factor", "lower", "upper", "permute", "spmv", "vector", "tail")
 
 _lib = None
 

@@ -33,13 +33,14 @@ constexpr int kReduceBlocks = 592;     // 4 per SM on a 148-SM part; fixed so su
 __global__ void arm_factor_kernel(int32_t* counters, int32_t* failed_row) {
   counters[0] = 0;
   counters[1] = 0;
+  counters[2] = 0;
   *failed_row = INT_MAX;
 }
 __global__ void arm_solve_kernel(int32_t* counters, int32_t* failed_upper) {
-  counters[2] = 0;  // lower ticket
-  counters[3] = 0;  // upper ticket
-  counters[4] = 0;  // lower rows finished
-  counters[5] = 0;  // upper rows finished
+  counters[4] = 0;  // lower ticket
+  counters[5] = 0;  // upper ticket
+  counters[6] = 0;  // lower rows finished
+  counters[7] = 0;  // upper rows finished
   *failed_upper = -1;
 }
 
@@ -62,9 +63,18 @@ struct b200lu_handle {
   // device: pattern + schedule
   int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_diag = nullptr;
   int32_t *d_small_rows = nullptr, *d_big_rows = nullptr, *d_lower_order = nullptr,
-          *d_upper_order = nullptr;
+          *d_upper_order = nullptr, *d_trivial_rows = nullptr;
   int64_t* d_pair_row_ptr = nullptr;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;      // triangular sweeps
+  // split sweeps (default mode): device image of the two TailPlans
+  struct TailDev {
+    int32_t rows = 0, head_claims = 0, head_publish = 0;
+    TailRow* row = nullptr;
+    TailEntry* entries = nullptr;
+    RowMeta* head_meta = nullptr;
+    int32_t* head_part_k = nullptr;
+  } lower_tail, upper_tail;
+  double* d_partial = nullptr;
   FactorMeta *d_small_meta = nullptr, *d_big_meta = nullptr;    // refactorization queues
   ScheduleTuning tune;
   void* d_dest = nullptr;
@@ -77,7 +87,7 @@ struct b200lu_handle {
   double *d_a_vals = nullptr, *d_work = nullptr, *d_values = nullptr;
   double *d_w = nullptr, *d_t1 = nullptr, *d_t2 = nullptr;
   double *d_in = nullptr, *d_in2 = nullptr, *d_out = nullptr;  // host<->device staging
-  int32_t* d_counters = nullptr;  // [0,1] factor tickets, [2,3] lower/upper tickets, [4,5] rows finished
+  int32_t* d_counters = nullptr;  // [0..2] factor tickets, [4,5] lower/upper tickets, [6,7] rows finished
   int32_t* d_failed = nullptr;    // [0] factor (atomicMin), [1] upper (atomicMax)
   double* d_scal = nullptr;       // scalar results of reductions
   double* d_partials = nullptr;
@@ -190,6 +200,12 @@ b200lu_status launch_factor(H* h, int64_t* failed_row) {
   if (h->n == 0) return B200LU_OK;
   arm_factor_kernel<<<1, 1, 0, h->stream>>>(h->d_counters, h->d_failed);
   ST_TRY(check_launch(h, "arm_factor_kernel"));
+  if (!h->sched.trivial_rows.empty()) {
+    const int32_t cnt = static_cast<int32_t>(h->sched.trivial_rows.size());
+    trivial_pivot_kernel<<<blocks_for(cnt, 256), 256, 0, h->stream>>>(cnt, h->d_trivial_rows, h->d_diag, h->d_work,
+                                                                      h->pivot_floor, h->d_failed);
+    ST_TRY(check_launch(h, "trivial_pivot_kernel"));
+  }
   FactorArgs a;
   a.n_small = static_cast<int32_t>(h->sched.small_rows.size());
   a.n_big = static_cast<int32_t>(h->sched.big_rows.size());
@@ -234,6 +250,9 @@ b200lu_status launch_factor(H* h, int64_t* failed_row) {
 TriArgs tri_args(H* h, const RowMeta* meta, const double* y, double* x, int counter_slot) {
   TriArgs a;
   a.n = static_cast<int32_t>(h->n);
+  a.n_publish = a.n;
+  a.part_k = nullptr;
+  a.partial = nullptr;
   a.meta = meta;
   a.col = h->d_col;
   a.diag = h->d_diag;
@@ -246,19 +265,95 @@ TriArgs tri_args(H* h, const RowMeta* meta, const double* y, double* x, int coun
   return a;
 }
 
-b200lu_status launch_lower(H* h, const double* y, double* x) {
-  PhaseScope ps(h, B200LU_PHASE_LOWER);
-  tri_kernel<false, false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 2));
-  return check_launch(h, "tri_kernel<lower>");
+TailArgs tail_args(H* h, const H::TailDev& t, const double* init, double* x) {
+  TailArgs a;
+  a.rows = t.rows;
+  a.row = t.row;
+  a.entries = t.entries;
+  a.values = h->d_values;
+  a.init = init;
+  a.x = x;
+  a.failed_row = h->d_failed + 1;
+  return a;
 }
-b200lu_status launch_upper(H* h, const double* y, double* x) {
-  PhaseScope ps(h, B200LU_PHASE_UPPER);
-  if (h->strict_order) {
-    tri_kernel<true, false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 3));
-  } else {
-    tri_kernel<true, true><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 3));
+
+constexpr int kTailCluster = 8;  // CTAs per tail cluster (portable maximum)
+
+template <bool kUpper>
+b200lu_status launch_tail(H* h, const TailArgs& args) {
+  cudaLaunchConfig_t cfg{};
+  static const int cluster = [] {
+    const char* e = std::getenv("B200LU_TAIL_CLUSTER");
+    const int c = e ? std::atoi(e) : kTailCluster;
+    return c >= 1 && c <= 8 ? c : kTailCluster;
+  }();
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(args.rows) * sizeof(double);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU_TRY(h, cudaLaunchKernelEx(&cfg, tail_kernel<kUpper>, args));
+  return check_launch(h, kUpper ? "tail_kernel<upper>" : "tail_kernel<lower>");
+}
+
+// L sweep. Strict order (or no narrow tail): the whole sweep in the sync-free kernel. Default:
+// head rows + the tail rows' prefix sums in the sync-free kernel, then the tail inside one CTA.
+b200lu_status launch_lower(H* h, const double* y, double* x) {
+  const H::TailDev& t = h->lower_tail;
+  if (h->strict_order || t.rows == 0) {
+    PhaseScope ps(h, B200LU_PHASE_LOWER);
+    TriArgs a = tri_args(h, h->d_lower_meta, y, x, 4);
+    tri_kernel<false, false, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    return check_launch(h, "tri_kernel<lower>");
   }
-  return check_launch(h, "tri_kernel<upper>");
+  const double* init = y;
+  if (t.head_publish > 0) {
+    PhaseScope ps(h, B200LU_PHASE_LOWER);
+    TriArgs a = tri_args(h, t.head_meta, y, x, 4);
+    a.n = t.head_claims;
+    a.n_publish = t.head_publish;
+    a.part_k = t.head_part_k;
+    a.partial = h->d_partial;
+    tri_kernel<false, false, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    ST_TRY(check_launch(h, "tri_kernel<lower head>"));
+    init = h->d_partial;
+  }  // else: no head rows, every prefix is empty and the partial sums are y itself
+  PhaseScope ps(h, B200LU_PHASE_TAIL);
+  return launch_tail<false>(h, tail_args(h, t, init, x));
+}
+
+// U sweep: the narrow part comes FIRST in dependency order (the last rows of the matrix).
+b200lu_status launch_upper(H* h, const double* y, double* x) {
+  const H::TailDev& t = h->upper_tail;
+  if (h->strict_order || t.rows == 0) {
+    PhaseScope ps(h, B200LU_PHASE_UPPER);
+    TriArgs a = tri_args(h, h->d_upper_meta, y, x, 5);
+    if (h->strict_order) {
+      tri_kernel<true, false, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    } else {
+      tri_kernel<true, true, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    }
+    return check_launch(h, "tri_kernel<upper>");
+  }
+  {
+    PhaseScope ps(h, B200LU_PHASE_TAIL);
+    ST_TRY(launch_tail<true>(h, tail_args(h, t, y, x)));
+  }
+  if (t.head_claims > 0) {
+    PhaseScope ps(h, B200LU_PHASE_UPPER);
+    TriArgs a = tri_args(h, t.head_meta, y, x, 5);
+    a.n = t.head_claims;
+    a.n_publish = t.head_claims;
+    tri_kernel<true, true, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    ST_TRY(check_launch(h, "tri_kernel<upper head>"));
+  }
+  return B200LU_OK;
 }
 
 // Device-to-device solve_system (src/trisolve.cpp:90-119). Does not synchronise; an exactly
@@ -660,6 +755,8 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   if (const char* e = std::getenv("B200LU_SOLVE_LOOKAHEAD_LEVELS")) h->tune.solve_lookahead_levels = std::atoll(e);
   if (const char* e = std::getenv("B200LU_SOLVE_MIN_WINDOW")) h->tune.solve_min_window = std::atoll(e);
   if (const char* e = std::getenv("B200LU_SOLVE_MAX_WINDOW")) h->tune.solve_max_window = std::atoll(e);
+  if (const char* e = std::getenv("B200LU_TAIL_WIDTH")) h->tune.tail_width = std::atoll(e);
+  if (const char* e = std::getenv("B200LU_TAIL_CAPACITY")) h->tune.tail_capacity = std::min<int64_t>(std::atoll(e), 24576);
   const std::string err = build_schedule(*sym, h->tune, h->sched);
   if (!err.empty()) {
     h->last_error = err;
@@ -683,11 +780,33 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   ST_TRY(dev_upload(h, &h->d_diag, S.diag));
   ST_TRY(dev_upload(h, &h->d_small_rows, S.small_rows));
   ST_TRY(dev_upload(h, &h->d_big_rows, S.big_rows));
+  ST_TRY(dev_upload(h, &h->d_trivial_rows, S.trivial_rows));
   ST_TRY(dev_upload(h, &h->d_lower_order, S.lower_order));
   ST_TRY(dev_upload(h, &h->d_upper_order, S.upper_order));
   ST_TRY(dev_upload(h, &h->d_pair_row_ptr, S.pair_row_ptr));
   ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
   ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
+  {
+    auto upload_tail = [&](const TailPlan& p, H::TailDev& d) -> b200lu_status {
+      d.rows = static_cast<int32_t>(p.rows);
+      if (p.rows == 0) return B200LU_OK;
+      d.head_claims = static_cast<int32_t>(p.head_meta.size());
+      d.head_publish = static_cast<int32_t>(p.head_publish);
+      ST_TRY(dev_upload(h, &d.row, p.row));
+      ST_TRY(dev_upload(h, &d.entries, p.entries));
+      ST_TRY(dev_upload(h, &d.head_meta, p.head_meta));
+      ST_TRY(dev_upload(h, &d.head_part_k, p.head_part_k));
+      return B200LU_OK;
+    };
+    ST_TRY(upload_tail(S.lower_tail, h->lower_tail));
+    ST_TRY(upload_tail(S.upper_tail, h->upper_tail));
+    ST_TRY(dev_alloc(h, &h->d_partial, n));
+    const int tail_smem = static_cast<int>(std::max(S.lower_tail.rows, S.upper_tail.rows) * sizeof(double));
+    if (tail_smem > 0) {
+      CU_TRY(h, cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem));
+      CU_TRY(h, cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem));
+    }
+  }
   {
     auto factor_meta = [&S](const std::vector<int32_t>& rows) {
       std::vector<FactorMeta> m(rows.size());
@@ -703,6 +822,10 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
 
   // scatter: inverse map (slot -> source entry), scale only on the matching path
   {
+    if (nnzA >= kTrivialBit) {
+      h->last_error = "nnz(A) exceeds the 2^30 entries the scatter map encoding supports";
+      return B200LU_INVALID_ARGUMENT;
+    }
     std::vector<int32_t> src_of_slot(nnzF, -1);
     for (int64_t k = 0; k < nnzA; ++k) {
       const int64_t s = sym->scatter_map[k];
@@ -711,6 +834,11 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
         return B200LU_INVALID_ARGUMENT;
       }
       src_of_slot[s] = static_cast<int32_t>(k);
+    }
+    for (int32_t i : S.trivial_rows) {  // slots the scatter pass publishes directly (factor.cuh, K1)
+      for (int32_t s = S.row_ptr[i]; s < S.row_ptr[i + 1]; ++s) {
+        src_of_slot[s] = src_of_slot[s] >= 0 ? (src_of_slot[s] | kTrivialBit) : kTrivialFill;
+      }
     }
     ST_TRY(dev_upload(h, &h->d_src_of_slot, src_of_slot));
     if (h->has_match) {
@@ -811,12 +939,16 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   }
   h->factor_grid = prop.multiProcessorCount * occ;
   int occ_tri = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri, tri_kernel<false, false>, 256, 0));
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri, tri_kernel<false, false, false>, 256, 0));
   int occ_tri_u = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_u, tri_kernel<true, false>, 256, 0));
-  int occ_tri_d = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_d, tri_kernel<true, true>, 256, 0));
-  occ_tri_u = std::min(occ_tri_u, occ_tri_d);
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri_u, tri_kernel<true, false, false>, 256, 0));
+  for (int v = 0; v < 3; ++v) {
+    int o = 0;
+    if (v == 0) CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tri_kernel<true, true, false>, 256, 0));
+    if (v == 1) CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tri_kernel<true, true, true>, 256, 0));
+    if (v == 2) CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tri_kernel<false, false, true>, 256, 0));
+    occ_tri_u = std::min(occ_tri_u, o);
+  }
   h->tri_grid = prop.multiProcessorCount * std::max(1, std::min(occ_tri, occ_tri_u));
   CU_TRY(h, cudaStreamSynchronize(h->stream));
   h->last_error.clear();
@@ -827,9 +959,11 @@ void b200lu_destroy(b200lu_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_small_rows, h->d_big_rows, h->d_lower_order,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_small_rows, h->d_big_rows, h->d_trivial_rows, h->d_lower_order,
                   h->d_upper_order, h->d_pair_row_ptr, h->d_lower_meta, h->d_upper_meta, h->d_small_meta,
-                  h->d_big_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p,
+                  h->d_big_meta, h->lower_tail.row, h->lower_tail.entries, h->lower_tail.head_meta,
+                  h->lower_tail.head_part_k, h->upper_tail.row, h->upper_tail.entries, h->upper_tail.head_meta,
+                  h->upper_tail.head_part_k, h->d_partial, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p,
                   h->d_pq, h->d_row_scale, h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_a_vals, h->d_work,
                   h->d_values, h->d_w, h->d_t1, h->d_t2, h->d_in, h->d_in2, h->d_out, h->d_counters, h->d_failed,
                   h->d_scal, h->d_partials, h->d_ticket, h->d_V, h->d_Z, h->d_wv, h->d_r, h->d_cand, h->d_best,
@@ -1039,6 +1173,10 @@ b200lu_status b200lu_get_stats(const b200lu_handle* h, b200lu_stats* out) {
   out->big_rows = static_cast<int64_t>(h->sched.big_rows.size());
   out->device_bytes = h->device_bytes;
   out->alloc_events = h->alloc_events;
+  out->lower_tail_rows = h->sched.lower_tail.rows;
+  out->lower_tail_levels = h->sched.lower_tail.levels;
+  out->upper_tail_rows = h->sched.upper_tail.rows;
+  out->upper_tail_levels = h->sched.upper_tail.levels;
   return B200LU_OK;
 }
 
@@ -1064,6 +1202,10 @@ b200lu_status b200lu_schedule_probe(const b200lu_symbolic_view* sym, b200lu_stat
     stats->upper_levels = S.upper_levels;
     stats->max_row_len = S.max_row_len;
     stats->big_rows = static_cast<int64_t>(S.big_rows.size());
+    stats->lower_tail_rows = S.lower_tail.rows;
+    stats->lower_tail_levels = S.lower_tail.levels;
+    stats->upper_tail_rows = S.upper_tail.rows;
+    stats->upper_tail_levels = S.upper_tail.levels;
   }
   if (lower_order && S.n) std::memcpy(lower_order, S.lower_order.data(), sizeof(int32_t) * S.n);
   if (upper_order && S.n) std::memcpy(upper_order, S.upper_order.data(), sizeof(int32_t) * S.n);

@@ -56,18 +56,44 @@ __device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
 
 // Throttle of a sync-free sweep: a claimed row sleeps until `start` rows of the sweep have
 // finished (schedule.hpp, fill_start_thresholds). One lane polls one counter, with a sleep
-// proportional to how far away the row still is.
-__device__ __forceinline__ void wait_for_start(const int32_t* finished, int32_t start, int lane) {
-  if (start > 0) {
+// proportional to how far away the row still is; `seen` caches the last value read (the
+// counter only grows), so rows whose threshold is already known to be met cost nothing.
+__device__ __forceinline__ void wait_for_start(const int32_t* finished, int32_t start, int lane, int32_t& seen) {
+  if (start > seen) {
+    int32_t c = 0;
     if (lane == 0) {
-      int32_t c = ld_l2_s32(finished);
+      c = ld_l2_s32(finished);
       while (c < start) {
         __nanosleep(min(4000, max(64, (start - c) * 4)));
         c = ld_l2_s32(finished);
       }
     }
-    __syncwarp();
+    seen = __shfl_sync(0xffffffffu, c, 0);
   }
+}
+
+// Read-only loads pinned in program order (asm volatile): used where a software pipeline issues
+// the next item's loads early and the compiler must not sink them to their first use.
+__device__ __forceinline__ double ldg_pinned(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return __longlong_as_double(static_cast<long long>(v));
+}
+__device__ __forceinline__ int2 ldg_pinned(const int2* p) {
+  int2 v;
+  asm volatile("ld.global.nc.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ldg_pinned(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+// Plain (coherent) pinned load for data written by an earlier kernel on the same stream.
+__device__ __forceinline__ double ld_pinned(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return __longlong_as_double(static_cast<long long>(v));
 }
 
 // a - b*c with two roundings (the reference's x86-64 baseline build has no FMA

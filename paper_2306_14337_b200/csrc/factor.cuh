@@ -11,9 +11,14 @@ namespace b200lu {
 // out[scatter_map[k]] = A.values[k] * scatter_scale[k].
 //
 // One fused pass in gather form: slot s reads its source entry through the inverse map
-// (src_of_slot[s] == -1 marks a fill slot, which becomes exactly 0), so every store is
+// (src_of_slot[s] < 0 marks a fill slot, which becomes exactly 0), so every store is
 // coalesced and no slot is written twice. The same pass re-arms `values` with the pending
-// marker that the refactorization kernel's waiters test for.
+// marker that the refactorization kernel's waiters test for — except in rows without a
+// strict-lower entry (76 % of the rows of a KKT system after AMD): elimination leaves such a row
+// unchanged (src/numeric.cpp:36 never iterates), so its scattered values ARE its factor
+// values and are published right here; the refactorization kernel never sees those rows.
+constexpr int32_t kTrivialBit = 0x40000000;  // src_of_slot flag: slot of a row without pivots
+constexpr int32_t kTrivialFill = -2;         // fill slot of such a row (-1: fill slot of any other row)
 __global__ void __launch_bounds__(256)
 scatter_kernel(int64_t nnz_factors, const int32_t* __restrict__ src_of_slot,
                const double* __restrict__ a_values, const double* __restrict__ scatter_scale,
@@ -22,15 +27,27 @@ scatter_kernel(int64_t nnz_factors, const int32_t* __restrict__ src_of_slot,
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < nnz_factors;
        s += stride) {
-    const int32_t k = __ldg(src_of_slot + s);
+    const int32_t code = __ldg(src_of_slot + s);
+    const bool trivial = code >= 0 ? (code & kTrivialBit) != 0 : code == kTrivialFill;
     double v = 0.0;
-    if (k >= 0) {
+    if (code >= 0) {
+      const int32_t k = code & ~kTrivialBit;
       v = __ldg(a_values + k);
       if (scatter_scale != nullptr) v = __dmul_rn(v, __ldg(scatter_scale + k));
     }
     work[s] = v;
-    values[s] = pending;
+    values[s] = trivial ? v : pending;
   }
+}
+
+// Pivot check of the rows K1 published directly (src/numeric.cpp:48 applies to every row).
+__global__ void __launch_bounds__(256)
+trivial_pivot_kernel(int32_t count, const int32_t* __restrict__ rows, const int32_t* __restrict__ diag,
+                     const double* __restrict__ work, double pivot_floor, int32_t* failed_row) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int32_t i = rows[t];
+  if (fabs(work[diag[i]]) <= pivot_floor) atomicMin(failed_row, i);
 }
 
 // --------------------------------------------------- update destination table

@@ -16,7 +16,7 @@ from tests.fixtures import csr_fixture, dense_fixture, golden_fixture, kkt_fixtu
 pytestmark = pytest.mark.gpu
 # The U sweep's summation order is selectable (include/b200lu.h, B200LU_FLAG_STRICT_ORDER): bitwise
 # comparisons of upper_solve / solve_system use the reference's order; the default (device
-# production order) is covered by test_default_u_sweep_order_* on the residual.
+# order) is covered by test_default_sweep_order_* on the residual.
 STRICT = rlu.FactorOptions(strict_order=True)
 needs_ref = pytest.mark.skipif(not rb.available(), reason="oracle/_ref/librlu_ref.so not built")
 
@@ -275,8 +275,9 @@ def test_no_device_allocation_after_create():
 
 @needs_ref
 @pytest.mark.parametrize("scaling", [False, True])
-def test_default_u_sweep_order_is_deterministic_and_as_accurate(scaling):
-    """Default options fold U rows in device production order: same terms, different rounding.
+def test_default_sweep_order_is_deterministic_and_as_accurate(scaling):
+    """Default options sum the sweeps' terms in device order (U rows last column first, the narrow
+    tail of the DAG inside one CTA with a fixed tree): same terms, different rounding.
     Tolerance: the direct residual may not exceed the reference-order residual by more than 4x
     (+1e-15 absolute), and two runs must agree bit for bit."""
     fx = kkt_fixture(6300, 2700, use_scaling=scaling)
@@ -286,7 +287,9 @@ def test_default_u_sweep_order_is_deterministic_and_as_accurate(scaling):
         rlu.refactorize(fs, fx.matrix(k))
         assert np.array_equal(f.values, fs.values)
         b = fx.rhs[k]
-        assert np.array_equal(rlu.lower_solve(f, b), rlu.lower_solve(fs, b))  # L sweep: always exact
+        lo_fast, lo_strict = rlu.lower_solve(f, b), rlu.lower_solve(fs, b)
+        assert np.array_equal(lo_strict, fx.oracle.lower_solve(fs.values, b))
+        assert np.allclose(lo_fast, lo_strict, rtol=0, atol=1e-9 * np.abs(lo_strict).max())
         x, xs = rlu.solve_system(f, b), rlu.solve_system(fs, b)
         assert np.array_equal(x, rlu.solve_system(f, b))
         assert np.array_equal(xs, fx.oracle.solve_system(fs.values, b)[0])

@@ -35,7 +35,8 @@ def main(n=20000, band=1):
         st = f.stats
         ok = bool(np.array_equal(f.values, fx.oracle.factorize(fx.values[0])[0]))
         print(json.dumps({"n": n, "band": band, "strict": strict, "levels": st["lower_levels"],
-                          "hop_ns": {p: round(1e6 * ph[p][0] / ph[p][1] / st["lower_levels"], 1) for p in ("factor", "lower", "upper")},
+                          "hop_ns": {p: round(1e6 * ph[p][0] / max(ph[p][1], 1) / st["lower_levels"], 1) for p in ("factor", "lower", "upper", "tail")},
+                          "launches": {p: ph[p][1] for p in ph}, "tail_rows": st["lower_tail_rows"],
                           "lu_bitwise": ok}))
         f.close()
 
