@@ -74,6 +74,11 @@ typedef struct {
   void* stream;       /* cudaStream_t to run on; NULL = the handle creates its own */
   int refine_capacity; /* largest RefineConfig.max_iterations this handle will see (Krylov storage); 0 = 20 */
   int flags;           /* B200LU_FLAG_* */
+  int concurrency;     /* handles expected to run at the same time on this device (scenario batches:
+                          one handle + stream per in-flight system). 0 or 1 = the handle may fill the
+                          GPU. With c > 1 every persistent grid is sized to 1/c of the device and all
+                          claim orders are dynamic, so kernels of different handles can share the SMs
+                          in any interleaving without waiting on each other's residency. */
 } b200lu_options;
 
 /* Summation order of the triangular sweeps (lower_core / upper_core, src/trisolve.cpp:28-68).

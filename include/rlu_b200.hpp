@@ -64,7 +64,8 @@ struct FactorOptions {  // include/rlu/numeric.hpp:12-15 (+ placement)
   int device = 0;
   void* stream = nullptr;
   int refine_capacity = 20;
-  bool strict_order = false;  // U sweep in the reference's summation order
+  bool strict_order = false;  // sweeps in the reference's summation order
+  int concurrency = 1;        // handles sharing the device at the same time
 };
 
 struct RefineConfig {  // include/rlu/refine.hpp:13-17
@@ -91,6 +92,7 @@ class NumericFactors {
     o.stream = opt.stream;
     o.refine_capacity = opt.refine_capacity;
     o.flags = opt.strict_order ? B200LU_FLAG_STRICT_ORDER : 0;
+    o.concurrency = opt.concurrency;
     b200lu_handle* h = nullptr;
     const b200lu_status st = b200lu_create(&sym, &o, &h);
     if (st != B200LU_OK) {

@@ -25,7 +25,7 @@ class SymbolicView(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("pivot_floor", dbl), ("device", i32), ("stream", vp), ("refine_capacity", i32),
-                ("flags", i32)]
+                ("flags", i32), ("concurrency", i32)]
 
 
 class RefineConfig(C.Structure):

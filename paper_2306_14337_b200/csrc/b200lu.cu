@@ -52,7 +52,8 @@ struct b200lu_handle {
   bool owns_stream = false;
   double pivot_floor = 1e-30;
   int refine_capacity = 20;
-  bool strict_order = false;  // U sweep folds in the reference's ascending column order
+  bool strict_order = false;  // sweeps fold in the reference's ascending column order
+  int concurrency = 1;        // handles sharing the device; > 1: partial grids, dynamic claim order only
 
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
@@ -98,6 +99,7 @@ struct b200lu_handle {
   double* h_scal = nullptr;  // pinned
   int32_t* h_failed = nullptr;  // pinned
 
+  void (*factor_fn)(FactorArgs) = nullptr;
   int factor_grid = 0, tri_grid = 0;
   size_t factor_smem = 0;
   int big_slot = 0;
@@ -225,11 +227,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_row) {
   a.failed_row = h->d_failed;
   {
     PhaseScope ps(h, B200LU_PHASE_FACTOR);
-    if (h->dest16) {
-      factor_kernel<uint16_t, kFactorWarps><<<h->factor_grid, kFactorWarps * 32, h->factor_smem, h->stream>>>(a);
-    } else {
-      factor_kernel<uint32_t, kFactorWarps><<<h->factor_grid, kFactorWarps * 32, h->factor_smem, h->stream>>>(a);
-    }
+    h->factor_fn<<<h->factor_grid, kFactorWarps * 32, h->factor_smem, h->stream>>>(a);
   }
   ST_TRY(check_launch(h, "factor_kernel"));
   CU_TRY(h, cudaMemcpyAsync(h->h_failed, h->d_failed, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
@@ -320,7 +318,11 @@ b200lu_status launch_lower(H* h, const double* y, double* x) {
     a.n_publish = t.head_publish;
     a.part_k = t.head_part_k;
     a.partial = h->d_partial;
-    tri_kernel<false, false, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    if (h->concurrency > 1) {  // static claim order needs the whole grid resident
+      tri_kernel<false, false, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    } else {
+      tri_kernel<false, false, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    }
     ST_TRY(check_launch(h, "tri_kernel<lower head>"));
     init = h->d_partial;
   }  // else: no head rows, every prefix is empty and the partial sums are y itself
@@ -350,7 +352,11 @@ b200lu_status launch_upper(H* h, const double* y, double* x) {
     TriArgs a = tri_args(h, t.head_meta, y, x, 5);
     a.n = t.head_claims;
     a.n_publish = t.head_claims;
-    tri_kernel<true, true, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    if (h->concurrency > 1) {
+      tri_kernel<true, true, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    } else {
+      tri_kernel<true, true, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+    }
     ST_TRY(check_launch(h, "tri_kernel<upper head>"));
   }
   return B200LU_OK;
@@ -700,6 +706,7 @@ void b200lu_default_options(b200lu_options* opt) {
   opt->stream = nullptr;
   opt->refine_capacity = 20;  // include/rlu/refine.hpp:14
   opt->flags = 0;
+  opt->concurrency = 1;
 }
 
 const char* b200lu_status_string(b200lu_status s) {
@@ -742,6 +749,7 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   h->pivot_floor = opt.pivot_floor;
   h->refine_capacity = opt.refine_capacity > 0 ? std::min(opt.refine_capacity, 64) : 20;
   h->strict_order = (opt.flags & B200LU_FLAG_STRICT_ORDER) != 0;
+  h->concurrency = std::max(1, opt.concurrency);
   CU_TRY(h, cudaSetDevice(h->device));
   if (opt.stream) {
     h->stream = static_cast<cudaStream_t>(opt.stream);
@@ -921,23 +929,31 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   for (int32_t i : S.big_rows) max_big = std::max<int64_t>(max_big, S.row_ptr[i + 1] - S.row_ptr[i]);
   h->big_slot = static_cast<int>(std::min<int64_t>((max_big + 63) / 64 * 64, kMaxBigSlot));
   h->factor_smem = (static_cast<size_t>(kFactorWarps) * h->tune.small_slot + h->big_slot) * sizeof(double);
-  int occ = 0;
-  if (h->dest16) {
-    CU_TRY(h, cudaFuncSetAttribute(factor_kernel<uint16_t, kFactorWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(h->factor_smem)));
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_kernel<uint16_t, kFactorWarps>,
-                                                            kFactorWarps * 32, h->factor_smem));
-  } else {
-    CU_TRY(h, cudaFuncSetAttribute(factor_kernel<uint32_t, kFactorWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(h->factor_smem)));
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_kernel<uint32_t, kFactorWarps>,
-                                                            kFactorWarps * 32, h->factor_smem));
+  // Kernel variant: pivots in flight per warp x resident CTAs per SM (register budget). The
+  // default is what DESIGN.md reports; B200LU_FACTOR_VARIANT selects others for experiments.
+  {
+    const char* e = std::getenv("B200LU_FACTOR_VARIANT");
+    const int variant = e ? std::atoi(e) : 0;
+    using Fn = void (*)(FactorArgs);
+    Fn f16[] = {factor_kernel<uint16_t, kFactorWarps, 4, 2>, factor_kernel<uint16_t, kFactorWarps, 4, 3>,
+                factor_kernel<uint16_t, kFactorWarps, 2, 4>, factor_kernel<uint16_t, kFactorWarps, 3, 3>,
+                factor_kernel<uint16_t, kFactorWarps, 6, 2>, factor_kernel<uint16_t, kFactorWarps, 2, 3>};
+    Fn f32[] = {factor_kernel<uint32_t, kFactorWarps, 4, 2>, factor_kernel<uint32_t, kFactorWarps, 4, 3>,
+                factor_kernel<uint32_t, kFactorWarps, 2, 4>, factor_kernel<uint32_t, kFactorWarps, 3, 3>,
+                factor_kernel<uint32_t, kFactorWarps, 6, 2>, factor_kernel<uint32_t, kFactorWarps, 2, 3>};
+    const int v = variant >= 0 && variant < 6 ? variant : 0;
+    h->factor_fn = h->dest16 ? f16[v] : f32[v];
   }
+  int occ = 0;
+  CU_TRY(h, cudaFuncSetAttribute(h->factor_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(h->factor_smem)));
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->factor_fn, kFactorWarps * 32, h->factor_smem));
   if (occ < 1) {
     h->last_error = "factor kernel does not fit on an SM";
     return B200LU_CUDA_ERROR;
   }
-  h->factor_grid = prop.multiProcessorCount * occ;
+  // With several handles sharing the device each takes its share of the resident CTAs.
+  h->factor_grid = std::max(prop.multiProcessorCount / 2, prop.multiProcessorCount * occ / h->concurrency);
   int occ_tri = 0;
   CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tri, tri_kernel<false, false, false>, 256, 0));
   int occ_tri_u = 0;
@@ -949,7 +965,8 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
     if (v == 2) CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tri_kernel<false, false, true>, 256, 0));
     occ_tri_u = std::min(occ_tri_u, o);
   }
-  h->tri_grid = prop.multiProcessorCount * std::max(1, std::min(occ_tri, occ_tri_u));
+  h->tri_grid = std::max(prop.multiProcessorCount / 2,
+                         prop.multiProcessorCount * std::max(1, std::min(occ_tri, occ_tri_u)) / h->concurrency);
   CU_TRY(h, cudaStreamSynchronize(h->stream));
   h->last_error.clear();
   return B200LU_OK;

@@ -128,9 +128,7 @@ struct FactorArgs {
   int32_t* failed_row;  // atomicMin target, initialised to INT32_MAX
 };
 
-constexpr int kPivotGroup = 4;
-
-template <typename DestT>
+template <typename DestT, int kPivotGroup>
 __device__ __forceinline__ void factor_row(const FactorArgs& a, const FactorMeta mt, double* row, int lane) {
   const unsigned full = 0xffffffffu;
   const int32_t i = mt.row, lo = mt.lo, dg = mt.dg, hi = mt.hi;
@@ -211,8 +209,8 @@ __device__ __forceinline__ void factor_row(const FactorArgs& a, const FactorMeta
   if (lane == 0 && fabs(row[nl]) <= a.pivot_floor) atomicMin(a.failed_row, i);
 }
 
-template <typename DestT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+template <typename DestT, int WARPS, int kPivotGroup, int kMinBlocks>
+__global__ void __launch_bounds__(WARPS * 32, kMinBlocks)
 factor_kernel(const FactorArgs a) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
@@ -230,7 +228,7 @@ factor_kernel(const FactorArgs a) {
       const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.big_meta) + r);
       const FactorMeta mt{m4.x, m4.y, m4.z, m4.w};
       double* row = (mt.hi - mt.lo) <= a.big_slot ? big_slot : a.work + mt.lo;
-      factor_row<DestT>(a, mt, row, lane);
+      factor_row<DestT, kPivotGroup>(a, mt, row, lane);
       __syncwarp();
     }
   }
@@ -240,7 +238,7 @@ factor_kernel(const FactorArgs a) {
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= a.n_small) break;
     const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.small_meta) + r);
-    factor_row<DestT>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, small_slot, lane);
+    factor_row<DestT, kPivotGroup>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, small_slot, lane);
     __syncwarp();
   }
 }

@@ -111,7 +111,8 @@ class FactorOptions:
     device: int = 0
     stream: int | None = None      # raw cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
     refine_capacity: int = 20
-    strict_order: bool = False     # U sweep in the reference's summation order (bit-identical x)
+    strict_order: bool = False     # sweeps in the reference's summation order (bit-identical x)
+    concurrency: int = 1           # handles sharing the device at the same time (scenario batches)
 
 
 @dataclass
@@ -159,6 +160,7 @@ class NumericFactors:
         o.stream = self.options.stream
         o.refine_capacity = self.options.refine_capacity
         o.flags = _capi.FLAG_STRICT_ORDER if self.options.strict_order else 0
+        o.concurrency = self.options.concurrency
         st = L.b200lu_create(C.byref(v), C.byref(o), C.byref(self._h))
         if st != _capi.OK:
             msg = L.b200lu_last_error(self._h).decode() if self._h else ""

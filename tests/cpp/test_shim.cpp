@@ -95,7 +95,7 @@ void run(const char* name, const std::function<void()>& fn) {
   std::printf("%s %s\n", failures == before ? "ok" : "FAILED", name);
 }
 
-const FactorOptions kStrict{1e-30, 0, nullptr, 20, true};
+const FactorOptions kStrict{1e-30, 0, nullptr, 20, true, 1};
 
 }  // namespace
 

@@ -472,3 +472,31 @@ def test_device_resident_vectors_match_host_path():
     assert dx.is_cuda and np.array_equal(dx.cpu().numpy(), rlu.solve_system(f, fx.rhs[0]))
     out = rlu.fgmres_refine(f, db, dx)
     assert out.x.is_cuda and _relres(fx, out.x.cpu().numpy(), fx.rhs[0]) <= 1e-14
+
+
+# ------------------------------------------------------------- scenario batches
+
+@needs_ref
+def test_scenario_batch_matches_single_handle_runs():
+    """independent scenarios sharing one pattern, several in flight on one GPU
+    (one handle + stream per in-flight system, FactorOptions.concurrency). Every scenario must
+    come out bit-identical to a lone run with the same options."""
+    from paper_2306_14337_b200.batch import ScenarioBatch
+    base = kkt_fixture(700, 300, num_systems=1)
+    scen = [kkt_fixture(700, 300, num_systems=1, y_seed=2 + s) for s in range(12)]
+    for s in scen:  # same topology_seed -> same pattern -> one analysis
+        assert np.array_equal(s.ci, base.ci) and np.array_equal(s.sym.col_indices, base.sym.col_indices)
+    mats = [rlu.CsrMatrix(base.n, base.n, base.ro, base.ci, s.values[0]) for s in scen]
+    rhs = [s.rhs[0] for s in scen]
+    batch = ScenarioBatch(base.sym, streams=4)
+    records, xs = batch.run(mats, rhs)
+    lone = rlu.NumericFactors(base.sym, rlu.FactorOptions(concurrency=4))
+    for s in range(len(scen)):
+        rlu.refactorize(lone, mats[s])
+        assert np.array_equal(lone.values, scen[s].oracle.factorize(scen[s].values[0])[0])
+        x0 = rlu.solve_system(lone, rhs[s])
+        out = rlu.fgmres_refine(lone, rhs[s], x0)
+        assert np.array_equal(xs[s], out.x)
+        assert records[s].scenario == s and records[s].failed_row == -1
+        assert records[s].refine_iters == out.iterations and records[s].relres_final <= 1e-14
+    batch.close()
