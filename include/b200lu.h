@@ -230,6 +230,74 @@ uint64_t b200lu_launch_count(const b200lu_handle* h);
 /* Blocks until everything queued on the handle's stream has finished. */
 b200lu_status b200lu_synchronize(b200lu_handle* h);
 
+/* ------------------------------------------------------------------------------------------
+ * Scenario batches (BASELINE config "batch of 256 independent scenario systems"):
+ * `batch` independent systems that share ONE symbolic analysis (same pattern, different values
+ * and right-hand sides), factorized and solved together. The reference has no batched entry
+ * point — cli::solve_sequence (src/cli.cpp:80-135) runs its systems one after another through
+ * the same four calls; each b200lu_batch_* function below is the corresponding single-system
+ * call applied to every scenario, with every scenario's arithmetic performed entry by entry in
+ * the reference's order: per-scenario L/U values, lower/upper/solve_system results and SpMV are
+ * bit-identical to the single-system CPU results.
+ *
+ * Array conventions: value arrays are [batch][nnz_source], vectors are [batch][n], both
+ * scenario-major and contiguous (scenario s starts at s * nnz_source resp. s * n); host or
+ * device pointers as selected by `on_device`. Per-scenario outputs (failed_rows, residuals,
+ * outcomes) hold `batch` entries. Internally every array is stored scenario-interleaved in
+ * groups of 32. */
+typedef struct b200lu_batch b200lu_batch;
+
+typedef struct {
+  int64_t batch, padded_batch;
+  int64_t unit_scenarios; /* scenarios a refactorization warp handles at once (8, 16 or 32) */
+  int64_t slot_entries;   /* row length a warp stages in shared memory; longer rows update in place */
+  int64_t factor_rows;    /* rows with at least one pivot */
+  int64_t staged_rows, staged_pairs; /* of those, rows (and their update pairs) staged in shared memory */
+  int64_t factor_grid, tri_grid;
+  int64_t n, nnz_factors, nnz_source, update_pairs, lower_levels, upper_levels;
+  int64_t device_bytes, alloc_events, launches;
+} b200lu_batch_info;
+
+/* NumericFactors::NumericFactors (src/numeric.cpp:8-12) for `batch` systems at once. Only
+ * pivot_floor, device, stream and refine_capacity of `opt` are used. */
+b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_options* opt,
+                                  int64_t batch, b200lu_batch** out);
+void b200lu_batch_destroy(b200lu_batch* h);
+const char* b200lu_batch_last_error(const b200lu_batch* h);
+/* pattern_equal guard (src/numeric.cpp:15-17), as b200lu_check_pattern. */
+b200lu_status b200lu_batch_check_pattern(const b200lu_batch* h, int64_t n, const int64_t* row_offsets,
+                                         const int64_t* col_indices);
+/* reset_values / factorize_scattered / refactorize (src/numeric.cpp:70-79) per scenario.
+ * failed_rows (may be NULL): per scenario the lowest failing permuted row, -1 when the scenario
+ * factorized. Returns B200LU_ZERO_PIVOT when any scenario failed; the others are valid. */
+b200lu_status b200lu_batch_reset_values(b200lu_batch* h, const double* a_values, int on_device);
+b200lu_status b200lu_batch_factorize_scattered(b200lu_batch* h, int64_t* failed_rows);
+b200lu_status b200lu_batch_refactorize(b200lu_batch* h, const double* a_values, int on_device,
+                                       int64_t* failed_rows);
+int b200lu_batch_valid(const b200lu_batch* h, int64_t scenario);
+/* NumericFactors::values of one scenario (nnz_factors doubles, host). */
+b200lu_status b200lu_batch_get_values(b200lu_batch* h, int64_t scenario, double* host_out);
+/* lower_solve / upper_solve / solve_system (src/trisolve.cpp:72-119) per scenario. Results of
+ * scenarios whose factorization failed are unspecified. */
+b200lu_status b200lu_batch_lower_solve(b200lu_batch* h, const double* y, double* x, int on_device);
+b200lu_status b200lu_batch_upper_solve(b200lu_batch* h, const double* y, double* x, int on_device,
+                                       int64_t* failed_rows);
+b200lu_status b200lu_batch_solve(b200lu_batch* h, const double* b, double* x, int on_device,
+                                 int64_t* failed_rows);
+/* relative_residual (src/sparse.cpp:283-288) per scenario; out holds `batch` doubles (host). */
+b200lu_status b200lu_batch_relative_residual(b200lu_batch* h, const double* x, const double* b,
+                                             int on_device, double* out);
+/* fgmres_refine (src/refine.cpp:39-142) per scenario, all scenarios advancing in lockstep;
+ * outcomes holds `batch` entries. */
+b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const double* x0,
+                                         double* x_out, int on_device, int use_preconditioner,
+                                         const b200lu_refine_config* cfg,
+                                         b200lu_refine_outcome* outcomes);
+b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out);
+b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled);
+b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset);
+b200lu_status b200lu_batch_synchronize(b200lu_batch* h);
+
 #ifdef __cplusplus
 }
 #endif

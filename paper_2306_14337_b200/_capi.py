@@ -44,6 +44,13 @@ class Stats(C.Structure):
                                    "lower_tail_levels", "upper_tail_rows", "upper_tail_levels")]
 
 
+class BatchInfo(C.Structure):
+    _fields_ = [(k, i64) for k in ("batch", "padded_batch", "unit_scenarios", "slot_entries", "factor_rows",
+                                   "staged_rows", "staged_pairs", "factor_grid", "tri_grid", "n", "nnz_factors",
+                                   "nnz_source", "update_pairs", "lower_levels", "upper_levels", "device_bytes",
+                                   "alloc_events", "launches")]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "b200lu_default_options": (None, [C.POINTER(Options)]),
@@ -76,6 +83,25 @@ EXPORTS = {
     "b200lu_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
     "b200lu_launch_count": (u64, [vp]),
     "b200lu_synchronize": (i32, [vp]),
+    # scenario batches
+    "b200lu_batch_create": (i32, [C.POINTER(SymbolicView), C.POINTER(Options), i64, C.POINTER(vp)]),
+    "b200lu_batch_destroy": (None, [vp]),
+    "b200lu_batch_last_error": (C.c_char_p, [vp]),
+    "b200lu_batch_check_pattern": (i32, [vp, i64, vp, vp]),
+    "b200lu_batch_reset_values": (i32, [vp, vp, i32]),
+    "b200lu_batch_factorize_scattered": (i32, [vp, vp]),
+    "b200lu_batch_refactorize": (i32, [vp, vp, i32, vp]),
+    "b200lu_batch_valid": (i32, [vp, i64]),
+    "b200lu_batch_get_values": (i32, [vp, i64, vp]),
+    "b200lu_batch_lower_solve": (i32, [vp, vp, vp, i32]),
+    "b200lu_batch_upper_solve": (i32, [vp, vp, vp, i32, vp]),
+    "b200lu_batch_solve": (i32, [vp, vp, vp, i32, vp]),
+    "b200lu_batch_relative_residual": (i32, [vp, vp, vp, i32, vp]),
+    "b200lu_batch_refine_fgmres": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
+    "b200lu_batch_get_info": (i32, [vp, C.POINTER(BatchInfo)]),
+    "b200lu_batch_set_timing": (i32, [vp, i32]),
+    "b200lu_batch_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
+    "b200lu_batch_synchronize": (i32, [vp]),
 }
 
 FLAG_STRICT_ORDER = 1

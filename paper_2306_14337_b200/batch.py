@@ -89,3 +89,214 @@ class ScenarioBatch:
             s, e = errors[0]
             raise RuntimeError(f"scenario {s} failed: {e}") from e
         return records, xs
+
+
+# ----------------------------------------------------------------------------------------------
+# Interleaved scenario batches: ONE handle, all scenarios factorized and solved together
+# (include/b200lu.h, b200lu_batch_*; kernels in csrc/batch.cuh).
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi
+
+
+def _symbolic_view(sym: rlu.SymbolicFactors):
+    v = _capi.SymbolicView()
+    v.n = sym.n
+    v.nnz_factors = int(sym.row_offsets[-1]) if len(sym.row_offsets) else 0
+    v.nnz_source = len(sym.scatter_map)
+    v.row_offsets, v.col_indices, v.diag_pos = (a.ctypes.data for a in (sym.row_offsets, sym.col_indices, sym.diag_pos))
+    v.scatter_map, v.scatter_scale, v.amd_forward = (a.ctypes.data for a in (sym.scatter_map, sym.scatter_scale, sym.amd_forward))
+    v.source_row_offsets, v.source_col_indices = sym.src_row_offsets.ctypes.data, sym.src_col_indices.ctypes.data
+    if sym.col_perm_forward is not None:
+        v.col_perm_forward = sym.col_perm_forward.ctypes.data
+        v.row_scale = sym.row_scale.ctypes.data
+        v.col_scale = sym.col_scale.ctypes.data
+    return v
+
+
+class BatchedFactors:
+    """`batch` NumericFactors (include/rlu/numeric.hpp:22-31) over one SymbolicFactors, stored
+    scenario-interleaved on the device. Value arrays are [batch, nnz(A)], vectors [batch, n]
+    (numpy arrays, or contiguous float64 CUDA tensors used in place). Every scenario's L/U values,
+    triangular solves and SpMV are bit-identical to the reference's single-system results."""
+
+    def __init__(self, sym: rlu.SymbolicFactors, batch: int, options: rlu.FactorOptions | None = None):
+        self.symbolic = sym
+        self.batch = int(batch)
+        self.options = options or rlu.FactorOptions()
+        self._h = C.c_void_p()
+        L = _capi.lib()
+        v = _symbolic_view(sym)
+        o = _capi.Options()
+        L.b200lu_default_options(C.byref(o))
+        o.pivot_floor = self.options.pivot_floor
+        o.device = self.options.device
+        o.stream = self.options.stream
+        o.refine_capacity = self.options.refine_capacity
+        st = L.b200lu_batch_create(C.byref(v), C.byref(o), self.batch, C.byref(self._h))
+        if st != _capi.OK:
+            msg = L.b200lu_batch_last_error(self._h).decode() if self._h else ""
+            if self._h:
+                L.b200lu_batch_destroy(self._h)
+                self._h = C.c_void_p()
+            if st == _capi.NO_DEVICE:
+                raise rlu.DeviceError("no CUDA device: the b200lu path has no CPU fallback")
+            raise (rlu.DeviceError if st == _capi.CUDA_ERROR else rlu.Error)(
+                f"b200lu_batch_create: {L.b200lu_status_string(st).decode()}: {msg}")
+        self._verified = set()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _capi.lib().b200lu_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing ------------------------------------------------------------
+    def _check(self, st, failed=None):
+        if st == _capi.OK:
+            return
+        L = _capi.lib()
+        msg = L.b200lu_batch_last_error(self._h).decode() or L.b200lu_status_string(st).decode()
+        if st == _capi.ZERO_PIVOT:
+            rows = [] if failed is None else [int(r) for r in failed]
+            bad = [s for s, r in enumerate(rows) if r >= 0]
+            e = rlu.ZeroPivotError(msg, rows[bad[0]] if bad else -1)
+            e.rows = rows            # per scenario, -1 = factorized
+            e.scenarios = bad
+            raise e
+        if st == _capi.PATTERN_MISMATCH:
+            raise rlu.PatternMismatchError("matrix pattern differs from the analyzed pattern")
+        if st == _capi.DIMENSION:
+            raise rlu.DimensionError(msg)
+        if st in (_capi.CUDA_ERROR, _capi.NO_DEVICE):
+            raise rlu.DeviceError(msg)
+        raise rlu.Error(msg)
+
+    def _arr_in(self, a, width, what):
+        """[batch, width] array -> (pointer, on_device, keepalive)."""
+        if rlu._is_device_tensor(a):
+            import torch
+            if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != self.batch * width:
+                raise rlu.DimensionError(f"{what}: expected a contiguous float64 [{self.batch}, {width}] tensor")
+            return a.data_ptr(), 1, a
+        h = np.ascontiguousarray(a, dtype=np.float64)
+        if h.size != self.batch * width:
+            raise rlu.DimensionError(f"{what}: expected [{self.batch}, {width}] values, got {h.size}")
+        return h.ctypes.data, 0, h
+
+    def _vec_out(self, like):
+        n = self.symbolic.n
+        if rlu._is_device_tensor(like):
+            import torch
+            out = torch.empty((self.batch, n), dtype=torch.float64, device=like.device)
+            return out.data_ptr(), out
+        out = np.empty((self.batch, n), dtype=np.float64)
+        return out.ctypes.data, out
+
+    def check_pattern(self, row_offsets, col_indices):
+        """pattern_equal guard of scatter_values (src/numeric.cpp:15-17)."""
+        ro, ci = rlu._i64(row_offsets), rlu._i64(col_indices)
+        st = _capi.PATTERN_MISMATCH
+        if ro.size == self.symbolic.n + 1 and ci.size == len(self.symbolic.src_col_indices):
+            st = _capi.lib().b200lu_batch_check_pattern(self._h, self.symbolic.n, ro.ctypes.data, ci.ctypes.data)
+        self._check(st)
+
+    # -- the reference's calls, per scenario -----------------------------------
+    def reset_values(self, values):
+        p, dev, keep = self._arr_in(values, len(self.symbolic.scatter_map), "reset_values")
+        self._check(_capi.lib().b200lu_batch_reset_values(self._h, p, dev))
+
+    def factorize_scattered(self):
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        self._check(_capi.lib().b200lu_batch_factorize_scattered(self._h, failed.ctypes.data), failed)
+
+    def refactorize(self, values, raise_on_zero_pivot=True):
+        """refactorize (src/numeric.cpp:70-73) for every scenario. Returns the per-scenario failed
+        rows (-1 = factorized); raises ZeroPivotError (with .rows / .scenarios) unless told not to."""
+        p, dev, keep = self._arr_in(values, len(self.symbolic.scatter_map), "refactorize")
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        st = _capi.lib().b200lu_batch_refactorize(self._h, p, dev, failed.ctypes.data)
+        if st == _capi.ZERO_PIVOT and not raise_on_zero_pivot:
+            return failed
+        self._check(st, failed)
+        return failed
+
+    def valid(self, scenario: int) -> bool:
+        return bool(_capi.lib().b200lu_batch_valid(self._h, scenario))
+
+    def values(self, scenario: int) -> np.ndarray:
+        out = np.empty(int(self.symbolic.row_offsets[-1]) if self.symbolic.n else 0, dtype=np.float64)
+        self._check(_capi.lib().b200lu_batch_get_values(self._h, scenario, out.ctypes.data))
+        return out
+
+    def lower_solve(self, y):
+        p, dev, keep = self._arr_in(y, self.symbolic.n, "lower_solve")
+        po, out = self._vec_out(y)
+        self._check(_capi.lib().b200lu_batch_lower_solve(self._h, p, po, dev))
+        return out
+
+    def upper_solve(self, y):
+        p, dev, keep = self._arr_in(y, self.symbolic.n, "upper_solve")
+        po, out = self._vec_out(y)
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        self._check(_capi.lib().b200lu_batch_upper_solve(self._h, p, po, dev, failed.ctypes.data), failed)
+        return out
+
+    def solve_system(self, b):
+        p, dev, keep = self._arr_in(b, self.symbolic.n, "solve_system")
+        po, out = self._vec_out(b)
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        self._check(_capi.lib().b200lu_batch_solve(self._h, p, po, dev, failed.ctypes.data), failed)
+        return out
+
+    def relative_residual(self, x, b) -> np.ndarray:
+        px, dev, k1 = self._arr_in(x, self.symbolic.n, "relative_residual")
+        pb, dev2, k2 = self._arr_in(b, self.symbolic.n, "relative_residual")
+        if dev != dev2:
+            raise rlu.Error("relative_residual: x and b must both be host arrays or both device tensors")
+        out = np.empty(self.batch, dtype=np.float64)
+        self._check(_capi.lib().b200lu_batch_relative_residual(self._h, px, pb, dev, out.ctypes.data))
+        return out
+
+    def fgmres_refine(self, b, x0, config: rlu.RefineConfig | None = None, preconditioned: bool = True):
+        """fgmres_refine (src/refine.cpp:39-142) per scenario. Returns (x [batch, n], outcomes)."""
+        config = config or rlu.RefineConfig()
+        pb, dev, k1 = self._arr_in(b, self.symbolic.n, "fgmres_refine")
+        px, dev2, k2 = self._arr_in(x0, self.symbolic.n, "fgmres_refine")
+        if dev != dev2:
+            raise rlu.Error("refine: b and x0 must both be host arrays or both device tensors")
+        po, out = self._vec_out(b)
+        cfg = _capi.RefineConfig(config.max_iterations, config.tolerance)
+        ocs = (_capi.RefineOutcome * self.batch)()
+        self._check(_capi.lib().b200lu_batch_refine_fgmres(self._h, pb, px, po, dev, 1 if preconditioned else 0,
+                                                           C.byref(cfg), C.cast(ocs, C.c_void_p)))
+        outcomes = [rlu.RefineOutcome(out[s], int(o.iterations), list(o.residual_history[:o.history_len]),
+                                      bool(o.converged)) for s, o in enumerate(ocs)]
+        return out, outcomes
+
+    # -- reporting -------------------------------------------------------------
+    @property
+    def info(self) -> dict:
+        s = _capi.BatchInfo()
+        self._check(_capi.lib().b200lu_batch_get_info(self._h, C.byref(s)))
+        return {k: int(getattr(s, k)) for k, _ in _capi.BatchInfo._fields_}
+
+    def set_timing(self, enabled: bool = True):
+        self._check(_capi.lib().b200lu_batch_set_timing(self._h, 1 if enabled else 0))
+
+    def phase_times(self, reset: bool = True) -> dict:
+        n = len(_capi.PHASES)
+        ms, cnt = (C.c_double * n)(), (C.c_int64 * n)()
+        self._check(_capi.lib().b200lu_batch_get_phase_times(self._h, ms, cnt, 1 if reset else 0))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_capi.PHASES)}
+
+    def synchronize(self):
+        self._check(_capi.lib().b200lu_batch_synchronize(self._h))

@@ -1,0 +1,1034 @@
+// b200lu scenario batches — handle, host-side orchestration and the b200lu_batch_* C ABI
+// (include/b200lu.h). Kernels: batch.cuh. One handle owns B scenarios that share one symbolic
+// analysis; every scenario's arithmetic is the reference's single-system arithmetic
+// (src/numeric.cpp, src/trisolve.cpp, src/sparse.cpp), and the refinement control flow is
+// fgmres_refine (src/refine.cpp:39-142) evaluated per scenario in lockstep.
+#include "b200lu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "batch.cuh"
+#include "schedule.hpp"
+
+using namespace b200lu;
+
+namespace {
+constexpr int kBWarps = 8;
+constexpr int kScalSlots = 40;  // device->host scalar rows (each `padded` doubles)
+constexpr int kUpSlots = 64;    // host->device scalar rows
+constexpr int kMaxTimedLaunches = 4096;
+
+__global__ void barm_kernel(unsigned long long* tickets, int32_t* failed, int32_t padded, int32_t value) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 4) tickets[t] = 0ull;
+  if (t < padded) failed[t] = value;
+}
+
+__global__ void bgather_scenario_kernel(int64_t len, int64_t group_base, int lane_of, const double* __restrict__ src,
+                                        double* __restrict__ dst) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < len) dst[k] = src[(group_base + k) * 32 + lane_of];
+}
+}  // namespace
+
+struct b200lu_batch {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  double pivot_floor = 1e-30;
+  int refine_capacity = 20;
+
+  Schedule sched;
+  int64_t n = 0, nnz_factors = 0, nnz_source = 0;
+  int32_t batch = 0, padded = 0, groups = 0;
+  int unit = 8;          // scenarios per refactorization unit (S)
+  int32_t units = 0;     // padded / unit
+  int32_t slot_entries = 0;
+  bool has_match = false, dest16 = true;
+  std::vector<int64_t> src_row_offsets, src_col_indices;
+  std::vector<uint8_t> valid;  // per scenario
+  int32_t gen = 0;
+
+  int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_diag = nullptr, *d_trivial_rows = nullptr;
+  int64_t* d_pair_row_ptr = nullptr;
+  FactorMeta* d_factor_meta = nullptr;
+  int32_t n_factor_rows = 0;
+  RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
+  void* d_dest = nullptr;
+  int32_t* d_src_of_slot = nullptr;
+  double* d_scatter_scale = nullptr;
+  int32_t *d_p = nullptr, *d_pq = nullptr;
+  double *d_row_scale = nullptr, *d_col_scale = nullptr;
+  int32_t *d_a_row_ptr = nullptr, *d_a_col = nullptr;
+
+  double *d_a_int = nullptr, *d_values = nullptr;
+  int32_t* d_flags = nullptr;
+  int32_t* d_failed = nullptr;  // [2][padded]: factor (atomicMin), upper (atomicMax)
+  unsigned long long* d_tickets = nullptr;
+  double *d_stage_a = nullptr, *d_stage_in = nullptr, *d_stage_in2 = nullptr, *d_stage_out = nullptr, *d_gather = nullptr;
+  double *d_w = nullptr, *d_t1 = nullptr, *d_t2 = nullptr, *d_b = nullptr, *d_x0 = nullptr, *d_x = nullptr,
+         *d_r = nullptr, *d_wv = nullptr, *d_cand = nullptr, *d_best = nullptr, *d_V = nullptr, *d_Z = nullptr;
+  double *d_scal = nullptr, *d_up = nullptr, *d_partials = nullptr;
+  double *h_scal = nullptr, *h_up = nullptr;
+  int32_t* h_failed = nullptr;
+  int up_used = 0;
+
+  void (*factor_fn)(BFactorArgs) = nullptr;
+  int factor_grid = 0, tri_grid = 0;
+  size_t factor_smem = 0;
+
+  int64_t alloc_events = 0, device_bytes = 0;
+  uint64_t launches = 0;
+  std::string last_error;
+
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_start, ev_stop;
+  std::vector<int> ev_phase;
+  int ev_used = 0;
+};
+
+namespace {
+
+using H = b200lu_batch;
+
+#define CU_TRY(h, expr)                                                      \
+  do {                                                                       \
+    cudaError_t e__ = (expr);                                                \
+    if (e__ != cudaSuccess) {                                                \
+      (h)->last_error = std::string(#expr) + ": " + cudaGetErrorString(e__); \
+      return B200LU_CUDA_ERROR;                                              \
+    }                                                                        \
+  } while (0)
+
+#define ST_TRY(expr)                  \
+  do {                                \
+    b200lu_status s__ = (expr);       \
+    if (s__ != B200LU_OK) return s__; \
+  } while (0)
+
+template <typename T>
+b200lu_status dev_alloc(H* h, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CU_TRY(h, cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  ++h->alloc_events;
+  h->device_bytes += static_cast<int64_t>(count * sizeof(T));
+  return B200LU_OK;
+}
+
+template <typename T>
+b200lu_status dev_upload(H* h, T** p, const std::vector<T>& v) {
+  ST_TRY(dev_alloc(h, p, v.size()));
+  if (!v.empty()) {
+    CU_TRY(h, cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    CU_TRY(h, cudaStreamSynchronize(h->stream));
+  }
+  return B200LU_OK;
+}
+
+inline int blocks_for(int64_t n, int threads) { return static_cast<int>(std::max<int64_t>(1, (n + threads - 1) / threads)); }
+
+b200lu_status check_launch(H* h, const char* what) {
+  ++h->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return B200LU_CUDA_ERROR;
+  }
+  return B200LU_OK;
+}
+
+struct PhaseScope {
+  H* h;
+  int idx = -1;
+  PhaseScope(H* handle, int phase) : h(handle) {
+    if (h->timing && h->ev_used < kMaxTimedLaunches) {
+      idx = h->ev_used++;
+      h->ev_phase[idx] = phase;
+      cudaEventRecord(h->ev_start[idx], h->stream);
+    }
+  }
+  ~PhaseScope() {
+    if (idx >= 0) cudaEventRecord(h->ev_stop[idx], h->stream);
+  }
+};
+
+inline int64_t vec_elems(const H* h) { return h->n * h->padded; }
+inline int warp_blocks(const H* h) { return blocks_for(h->n * h->groups * 32, 256); }
+
+// ---- layout changes between the caller's scenario-major arrays and the interleaved storage
+
+b200lu_status to_interleaved(H* h, int64_t len, const double* src_dev, double* dst) {
+  if (len == 0) return B200LU_OK;
+  PhaseScope ps(h, B200LU_PHASE_PERMUTE);
+  dim3 grid(static_cast<unsigned>((len + 31) / 32), static_cast<unsigned>(h->groups));
+  interleave_kernel<<<grid, 256, 0, h->stream>>>(len, h->batch, src_dev, dst);
+  return check_launch(h, "interleave_kernel");
+}
+
+b200lu_status from_interleaved(H* h, int64_t len, const double* src, double* dst_dev) {
+  if (len == 0) return B200LU_OK;
+  PhaseScope ps(h, B200LU_PHASE_PERMUTE);
+  dim3 grid(static_cast<unsigned>((len + 31) / 32), static_cast<unsigned>(h->groups));
+  deinterleave_kernel<<<grid, 256, 0, h->stream>>>(len, h->batch, src, dst_dev);
+  return check_launch(h, "deinterleave_kernel");
+}
+
+// caller's [batch][n] vector (host or device) -> interleaved device vector
+b200lu_status vec_in(H* h, const double* p, int on_device, double* staging, double* dst) {
+  const double* src = p;
+  if (!on_device) {
+    CU_TRY(h, cudaMemcpyAsync(staging, p, static_cast<size_t>(h->n) * h->batch * sizeof(double), cudaMemcpyHostToDevice,
+                              h->stream));
+    src = staging;
+  }
+  return to_interleaved(h, h->n, src, dst);
+}
+
+// interleaved device vector -> caller's [batch][n] vector; synchronises
+b200lu_status vec_out(H* h, const double* src, double* p, int on_device) {
+  if (on_device) {
+    ST_TRY(from_interleaved(h, h->n, src, p));
+  } else {
+    ST_TRY(from_interleaved(h, h->n, src, h->d_stage_out));
+    CU_TRY(h, cudaMemcpyAsync(p, h->d_stage_out, static_cast<size_t>(h->n) * h->batch * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+  }
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  return B200LU_OK;
+}
+
+// ---- scalar traffic
+
+b200lu_status read_scalars(H* h, int first_slot, int slots) {
+  CU_TRY(h, cudaMemcpyAsync(h->h_scal + static_cast<size_t>(first_slot) * h->padded,
+                            h->d_scal + static_cast<size_t>(first_slot) * h->padded,
+                            static_cast<size_t>(slots) * h->padded * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  h->up_used = 0;  // every earlier upload has been consumed
+  return B200LU_OK;
+}
+
+// per-scenario scalars host -> device; returns the device row
+b200lu_status upload_scalars(H* h, const std::vector<double>& v, const double** dev) {
+  if (h->up_used >= kUpSlots) {
+    CU_TRY(h, cudaStreamSynchronize(h->stream));
+    h->up_used = 0;
+  }
+  double* hp = h->h_up + static_cast<size_t>(h->up_used) * h->padded;
+  double* dp = h->d_up + static_cast<size_t>(h->up_used) * h->padded;
+  for (int32_t s = 0; s < h->padded; ++s) hp[s] = v[std::min<int32_t>(s, h->batch - 1)];
+  CU_TRY(h, cudaMemcpyAsync(dp, hp, static_cast<size_t>(h->padded) * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  ++h->up_used;
+  *dev = dp;
+  return B200LU_OK;
+}
+
+double* scal(H* h, int slot) { return h->d_scal + static_cast<size_t>(slot) * h->padded; }
+const double* hscal(const H* h, int slot) { return h->h_scal + static_cast<size_t>(slot) * h->padded; }
+
+// ---- device stages
+
+b200lu_status launch_scatter(H* h) {
+  if (h->nnz_factors == 0) return B200LU_OK;
+  PhaseScope ps(h, B200LU_PHASE_SCATTER);
+  const int blocks = std::min<int64_t>(blocks_for(h->nnz_factors * h->groups * 32, 256), 148 * 32);
+  bscatter_kernel<<<blocks, 256, 0, h->stream>>>(h->nnz_factors, h->nnz_source, h->groups, h->d_src_of_slot, h->d_a_int,
+                                                 h->d_scatter_scale, h->d_values);
+  return check_launch(h, "bscatter_kernel");
+}
+
+b200lu_status launch_factor(H* h, int64_t* failed_rows) {
+  for (int32_t s = 0; failed_rows && s < h->batch; ++s) failed_rows[s] = -1;
+  if (h->n == 0) {
+    std::fill(h->valid.begin(), h->valid.end(), 1);
+    return B200LU_OK;
+  }
+  ++h->gen;
+  barm_kernel<<<blocks_for(std::max(h->padded, 4), 256), 256, 0, h->stream>>>(h->d_tickets, h->d_failed, h->padded, INT_MAX);
+  ST_TRY(check_launch(h, "barm_kernel"));
+  if (!h->sched.trivial_rows.empty()) {
+    const int32_t cnt = static_cast<int32_t>(h->sched.trivial_rows.size());
+    btrivial_pivot_kernel<<<blocks_for(static_cast<int64_t>(cnt) * h->groups * 32, 256), 256, 0, h->stream>>>(
+        cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
+    ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
+  }
+  if (h->n_factor_rows > 0) {
+    BFactorArgs a;
+    a.n_rows = h->n_factor_rows;
+    a.units = h->units;
+    a.slot_entries = h->slot_entries;
+    a.gen = h->gen;
+    a.meta = h->d_factor_meta;
+    a.row_ptr = h->d_row_ptr;
+    a.col = h->d_col;
+    a.diag = h->d_diag;
+    a.pair_row_ptr = h->d_pair_row_ptr;
+    a.dest = h->d_dest;
+    a.values = h->d_values;
+    a.nnz_factors = h->nnz_factors;
+    a.flags = h->d_flags;
+    a.pivot_floor = h->pivot_floor;
+    a.failed = h->d_failed;
+    a.ticket = h->d_tickets;
+    PhaseScope ps(h, B200LU_PHASE_FACTOR);
+    h->factor_fn<<<h->factor_grid, kBWarps * 32, h->factor_smem, h->stream>>>(a);
+    ST_TRY(check_launch(h, "bfactor_kernel"));
+  }
+  CU_TRY(h, cudaMemcpyAsync(h->h_failed, h->d_failed, static_cast<size_t>(h->padded) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  bool any = false;
+  for (int32_t s = 0; s < h->batch; ++s) {
+    const bool ok = h->h_failed[s] == INT_MAX;
+    h->valid[s] = ok ? 1 : 0;  // src/numeric.cpp:51-55: a failed system's factors stay invalid
+    if (!ok) {
+      any = true;
+      if (failed_rows) failed_rows[s] = h->h_failed[s];
+      h->last_error = "zero pivot at row " + std::to_string(h->h_failed[s]) + " of scenario " + std::to_string(s);
+    }
+  }
+  return any ? B200LU_ZERO_PIVOT : B200LU_OK;
+}
+
+BTriArgs tri_args(H* h, const RowMeta* meta, const double* y, double* x, int ticket_slot) {
+  BTriArgs a;
+  a.n = static_cast<int32_t>(h->n);
+  a.groups = h->groups;
+  a.meta = meta;
+  a.col = h->d_col;
+  a.diag = h->d_diag;
+  a.values = h->d_values;
+  a.nnz_factors = h->nnz_factors;
+  a.y = y;
+  a.x = x;
+  a.ticket = h->d_tickets + ticket_slot;
+  a.failed = h->d_failed + h->padded;
+  return a;
+}
+
+b200lu_status arm_solve(H* h) {
+  barm_kernel<<<blocks_for(std::max(h->padded, 4), 256), 256, 0, h->stream>>>(h->d_tickets, h->d_failed + h->padded,
+                                                                            h->padded, -1);
+  return check_launch(h, "barm_kernel");
+}
+
+b200lu_status launch_lower(H* h, const double* y, double* x) {
+  PhaseScope ps(h, B200LU_PHASE_LOWER);
+  btri_kernel<false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 1));
+  return check_launch(h, "btri_kernel<lower>");
+}
+
+b200lu_status launch_upper(H* h, const double* y, double* x) {
+  PhaseScope ps(h, B200LU_PHASE_UPPER);
+  btri_kernel<true><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 2));
+  return check_launch(h, "btri_kernel<upper>");
+}
+
+// solve_system (src/trisolve.cpp:90-119) on interleaved vectors; does not synchronise
+b200lu_status solve_int(H* h, const double* b, double* x) {
+  if (h->n == 0) return B200LU_OK;
+  ST_TRY(arm_solve(h));
+  {
+    PhaseScope ps(h, B200LU_PHASE_PERMUTE);
+    bpermute_in_kernel<<<warp_blocks(h), 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->groups, h->d_p,
+                                                              h->d_row_scale, b, h->d_w, h->d_t1, h->d_t2);
+    ST_TRY(check_launch(h, "bpermute_in_kernel"));
+  }
+  ST_TRY(launch_lower(h, h->d_w, h->d_t1));
+  ST_TRY(launch_upper(h, h->d_t1, h->d_t2));
+  PhaseScope ps(h, B200LU_PHASE_PERMUTE);
+  bpermute_out_kernel<<<warp_blocks(h), 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->groups, h->d_pq,
+                                                             h->d_col_scale, h->d_t2, x);
+  return check_launch(h, "bpermute_out_kernel");
+}
+
+b200lu_status collect_upper_failure(H* h, int64_t* failed_rows) {
+  for (int32_t s = 0; failed_rows && s < h->batch; ++s) failed_rows[s] = -1;
+  if (h->n == 0) return B200LU_OK;
+  CU_TRY(h, cudaMemcpyAsync(h->h_failed + h->padded, h->d_failed + h->padded, static_cast<size_t>(h->padded) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  bool any = false;
+  for (int32_t s = 0; s < h->batch; ++s) {
+    const int32_t f = h->h_failed[h->padded + s];
+    if (f >= 0 && h->valid[s]) {
+      any = true;
+      if (failed_rows) failed_rows[s] = f;
+      h->last_error = "zero diagonal at row " + std::to_string(f) + " of scenario " + std::to_string(s);
+    }
+  }
+  return any ? B200LU_ZERO_PIVOT : B200LU_OK;
+}
+
+b200lu_status any_valid(H* h, const char* who) {
+  for (uint8_t v : h->valid) {
+    if (v) return B200LU_OK;
+  }
+  h->last_error = std::string(who) + ": factors are not valid";  // src/trisolve.cpp:20
+  return B200LU_INVALID_FACTORS;
+}
+
+b200lu_status launch_residual(H* h, const double* x, const double* b, double* r, int slot) {
+  {
+    PhaseScope ps(h, B200LU_PHASE_SPMV);
+    dim3 grid(kBatchPartBlocks, static_cast<unsigned>(h->groups));
+    bresidual_kernel<<<grid, 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->nnz_source, h->d_a_row_ptr, h->d_a_col,
+                                                  h->d_a_int, x, b, r, h->d_partials);
+    ST_TRY(check_launch(h, "bresidual_kernel"));
+  }
+  PhaseScope ps(h, B200LU_PHASE_VECTOR);
+  bfinish_kernel<<<h->groups, 32, 0, h->stream>>>(2, h->padded, h->d_partials, scal(h, slot));
+  return check_launch(h, "bfinish_kernel");
+}
+
+b200lu_status launch_dot(H* h, const double* u, const double* v, int slot) {
+  PhaseScope ps(h, B200LU_PHASE_VECTOR);
+  dim3 grid(kBatchPartBlocks, static_cast<unsigned>(h->groups));
+  bdot_kernel<<<grid, 256, 0, h->stream>>>(static_cast<int32_t>(h->n), u, v, h->d_partials);
+  ST_TRY(check_launch(h, "bdot_kernel"));
+  bfinish_kernel<<<h->groups, 32, 0, h->stream>>>(1, h->padded, h->d_partials, scal(h, slot));
+  return check_launch(h, "bfinish_kernel");
+}
+
+b200lu_status launch_spmv(H* h, const double* x, double* y) {
+  PhaseScope ps(h, B200LU_PHASE_SPMV);
+  bspmv_kernel<<<warp_blocks(h), 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->groups, h->nnz_source, h->d_a_row_ptr,
+                                                      h->d_a_col, h->d_a_int, x, y);
+  return check_launch(h, "bspmv_kernel");
+}
+
+b200lu_status copy_dd(H* h, double* dst, const double* src) {
+  if (dst == src || h->n == 0) return B200LU_OK;
+  CU_TRY(h, cudaMemcpyAsync(dst, src, static_cast<size_t>(vec_elems(h)) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  return B200LU_OK;
+}
+
+enum { kSlotRes = 0, kSlotBn = 1, kSlotNorm = 2, kSlotH = 3, kSlotCoef = 8 };
+
+// fgmres_refine (src/refine.cpp:39-142) for every scenario in lockstep. Each scenario follows
+// the reference's control flow on its own scalars (early exit, breakdown, candidate only when
+// the estimate clears accept_below or on the last iteration, true residual, best-iterate rule);
+// a scenario that has finished keeps its best iterate and rides along with neutral scalars.
+b200lu_status fgmres_batch(H* h, const double* b, const double* x0, int use_precond, const b200lu_refine_config& cfg,
+                           b200lu_refine_outcome* out) {
+  const int64_t ne = vec_elems(h);
+  const int32_t n32 = static_cast<int32_t>(h->n);
+  const int32_t B = h->batch;
+  const int m = std::max(1, cfg.max_iterations);
+  const int wb = warp_blocks(h);
+  for (int32_t s = 0; s < B; ++s) {
+    out[s].iterations = 0;
+    out[s].converged = 0;
+    out[s].history_len = 0;
+  }
+  ST_TRY(copy_dd(h, h->d_best, x0));
+  if (h->n == 0) {
+    for (int32_t s = 0; s < B; ++s) {
+      out[s].residual_history[out[s].history_len++] = 0.0;
+      out[s].converged = 1;
+    }
+    return B200LU_OK;
+  }
+  ST_TRY(launch_residual(h, x0, b, h->d_r, kSlotRes));
+  ST_TRY(read_scalars(h, kSlotRes, 2));
+  std::vector<double> bnorm(B), beta(B), best_res(B), accept_below(B);
+  std::vector<uint8_t> active(B, 1);
+  int n_active = 0;
+  for (int32_t s = 0; s < B; ++s) {
+    const double bn = std::sqrt(hscal(h, kSlotBn)[s]);
+    bnorm[s] = bn > 0.0 ? bn : 1.0;
+    beta[s] = std::sqrt(hscal(h, kSlotRes)[s]);
+    best_res[s] = beta[s] / bnorm[s];
+    out[s].residual_history[out[s].history_len++] = best_res[s];
+    accept_below[s] = cfg.tolerance * bnorm[s];
+    if (best_res[s] <= cfg.tolerance) {
+      out[s].converged = 1;
+      active[s] = 0;
+    }
+    n_active += active[s];
+  }
+  if (n_active == 0) return B200LU_OK;
+
+  auto V = [&](int j) { return h->d_V + static_cast<size_t>(j) * ne; };
+  auto Z = [&](int j) { return h->d_Z + static_cast<size_t>(j) * ne; };
+  std::vector<double> tmp(B);
+  const double* dev = nullptr;
+  for (int32_t s = 0; s < B; ++s) tmp[s] = active[s] ? beta[s] : 1.0;
+  ST_TRY(upload_scalars(h, tmp, &dev));
+  {
+    PhaseScope ps(h, B200LU_PHASE_VECTOR);
+    bdivide_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, h->d_r, V(0));
+  }
+  ST_TRY(check_launch(h, "bdivide_kernel"));
+  int nV = 1;
+
+  std::vector<std::vector<std::vector<double>>> Hm(B);  // per scenario: columns after rotations
+  std::vector<std::vector<double>> g(B, std::vector<double>(static_cast<size_t>(m) + 1, 0.0)),
+      cs(B, std::vector<double>(m, 0.0)), sn(B, std::vector<double>(m, 0.0));
+  for (int32_t s = 0; s < B; ++s) g[s][0] = beta[s];
+
+  for (int i = 0; i < m && n_active > 0; ++i) {
+    if (use_precond) {
+      ST_TRY(solve_int(h, V(i), Z(i)));
+    } else {
+      ST_TRY(copy_dd(h, Z(i), V(i)));
+    }
+    ST_TRY(launch_spmv(h, Z(i), h->d_wv));
+    // cgs2_orthonormalize(V, w), src/refine.cpp:8-26
+    CU_TRY(h, cudaMemsetAsync(scal(h, kSlotCoef), 0, static_cast<size_t>(nV) * h->padded * sizeof(double), h->stream));
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = 0; j < nV; ++j) {
+        ST_TRY(launch_dot(h, V(j), h->d_wv, kSlotH));
+        {
+          PhaseScope ps(h, B200LU_PHASE_VECTOR);
+          bproject_out_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, scal(h, kSlotH), scal(h, kSlotCoef + j), V(j),
+                                                         h->d_wv);
+        }
+        ST_TRY(check_launch(h, "bproject_out_kernel"));
+      }
+    }
+    ST_TRY(launch_dot(h, h->d_wv, h->d_wv, kSlotNorm));
+    ST_TRY(read_scalars(h, kSlotNorm, kSlotCoef + nV - kSlotNorm));
+
+    std::vector<uint8_t> breakdown(B, 0), need_cand(B, 0), last(B, 0);
+    std::vector<double> estimate(B, 0.0);
+    bool any_new_v = false, any_cand = false;
+    for (int32_t s = 0; s < B; ++s) {
+      tmp[s] = 1.0;
+      if (!active[s]) continue;
+      const double norm = std::sqrt(hscal(h, kSlotNorm)[s]);
+      breakdown[s] = norm <= 1e-300;
+      std::vector<double> hcol(nV);
+      for (int j = 0; j < nV; ++j) hcol[j] = hscal(h, kSlotCoef + j)[s];
+      hcol.push_back(breakdown[s] ? 0.0 : norm);
+      if (!breakdown[s]) {
+        tmp[s] = norm;
+        any_new_v = true;
+      }
+      // Givens update, src/refine.cpp:89-107
+      for (int k = 0; k < i; ++k) {
+        const double t = hcol[k];
+        hcol[k] = cs[s][k] * t + sn[s][k] * hcol[k + 1];
+        hcol[k + 1] = -sn[s][k] * t + cs[s][k] * hcol[k + 1];
+      }
+      const double hii = hcol[i], hsub = hcol[i + 1];
+      const double gam = std::hypot(hii, hsub);
+      if (gam == 0.0) {
+        cs[s][i] = 1.0;
+        sn[s][i] = 0.0;
+      } else {
+        cs[s][i] = hii / gam;
+        sn[s][i] = hsub / gam;
+      }
+      hcol[i] = gam;
+      hcol[i + 1] = 0.0;
+      const double gi = g[s][i];
+      g[s][i] = cs[s][i] * gi;
+      g[s][i + 1] = -sn[s][i] * gi;
+      Hm[s].push_back(std::move(hcol));
+      out[s].iterations = i + 1;
+      estimate[s] = std::fabs(g[s][i + 1]);
+      out[s].residual_history[out[s].history_len++] = estimate[s] / bnorm[s];
+      last[s] = breakdown[s] || i == m - 1;
+      need_cand[s] = estimate[s] <= accept_below[s] || last[s];
+      any_cand = any_cand || need_cand[s];
+    }
+    if (any_new_v) {  // V(nV) = w / norm for the scenarios that continue
+      ST_TRY(upload_scalars(h, tmp, &dev));
+      {
+        PhaseScope ps(h, B200LU_PHASE_VECTOR);
+        bdivide_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, h->d_wv, V(nV));
+      }
+      ST_TRY(check_launch(h, "bdivide_kernel"));
+    }
+    if (any_cand) {
+      // src/refine.cpp:115-139: minimum-residual iterate, true residual, best-iterate rule
+      const int its = i + 1;
+      std::vector<std::vector<double>> y(its, std::vector<double>(B, 0.0));
+      for (int32_t s = 0; s < B; ++s) {
+        if (!need_cand[s]) continue;
+        std::vector<double> ys(its);
+        for (int row = its - 1; row >= 0; --row) {
+          double t = g[s][row];
+          for (int col = row + 1; col < its; ++col) t -= Hm[s][col][row] * ys[col];
+          ys[row] = t / Hm[s][row][row];
+        }
+        for (int col = 0; col < its; ++col) y[col][s] = ys[col];
+      }
+      ST_TRY(copy_dd(h, h->d_cand, x0));
+      for (int col = 0; col < its; ++col) {
+        ST_TRY(upload_scalars(h, y[col], &dev));
+        {
+          PhaseScope ps(h, B200LU_PHASE_VECTOR);
+          baxpy_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, Z(col), h->d_cand);
+        }
+        ST_TRY(check_launch(h, "baxpy_kernel"));
+      }
+      ST_TRY(launch_residual(h, h->d_cand, b, h->d_r, kSlotRes));
+      ST_TRY(read_scalars(h, kSlotRes, 1));
+      bool any_copy = false;
+      for (int32_t s = 0; s < B; ++s) {
+        tmp[s] = 0.0;
+        if (!need_cand[s]) continue;
+        const double res = std::sqrt(hscal(h, kSlotRes)[s]) / bnorm[s];
+        if (res < best_res[s]) {
+          best_res[s] = res;
+          tmp[s] = 1.0;
+          any_copy = true;
+        }
+        if (best_res[s] <= cfg.tolerance) {
+          out[s].converged = 1;
+          active[s] = 0;
+        } else if (last[s]) {
+          active[s] = 0;
+        } else {
+          accept_below[s] = estimate[s] * 0.5;
+        }
+      }
+      if (any_copy) {
+        ST_TRY(upload_scalars(h, tmp, &dev));
+        {
+          PhaseScope ps(h, B200LU_PHASE_VECTOR);
+          bcopy_masked_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, h->d_cand, h->d_best);
+        }
+        ST_TRY(check_launch(h, "bcopy_masked_kernel"));
+      }
+    }
+    if (any_new_v) ++nV;
+    n_active = 0;
+    for (int32_t s = 0; s < B; ++s) n_active += active[s];
+  }
+  return B200LU_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+const char* b200lu_batch_last_error(const b200lu_batch* h) { return h ? h->last_error.c_str() : ""; }
+
+b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_options* opt_in, int64_t batch,
+                                  b200lu_batch** out) {
+  if (!sym || !out || batch < 1 || batch > (1 << 20)) return B200LU_INVALID_ARGUMENT;
+  *out = nullptr;
+  b200lu_options opt;
+  b200lu_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  if (b200lu_device_count() <= opt.device) return B200LU_NO_DEVICE;
+  H* h = new H;
+  *out = h;
+  h->device = opt.device;
+  h->pivot_floor = opt.pivot_floor;
+  h->refine_capacity = opt.refine_capacity > 0 ? std::min(opt.refine_capacity, 64) : 20;
+  h->batch = static_cast<int32_t>(batch);
+  h->groups = (h->batch + 31) / 32;
+  h->padded = h->groups * 32;
+  h->valid.assign(batch, 0);
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (opt.stream) {
+    h->stream = static_cast<cudaStream_t>(opt.stream);
+  } else {
+    CU_TRY(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->owns_stream = true;
+  }
+  ScheduleTuning tune;
+  tune.tail_min_levels = int64_t{1} << 40;  // no on-chip tail split: the batched sweeps run whole
+  const std::string err = build_schedule(*sym, tune, h->sched);
+  if (!err.empty()) {
+    h->last_error = err;
+    return B200LU_INVALID_ARGUMENT;
+  }
+  const Schedule& S = h->sched;
+  const int64_t n = h->n = sym->n;
+  const int64_t nnzF = h->nnz_factors = sym->nnz_factors;
+  const int64_t nnzA = h->nnz_source = sym->nnz_source;
+  h->has_match = sym->col_perm_forward != nullptr;
+  if (nnzA >= (int64_t{1} << 31) - 64) {
+    h->last_error = "nnz(A) exceeds the int32 device index range";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  h->src_row_offsets.assign(sym->source_row_offsets, sym->source_row_offsets + n + 1);
+  h->src_col_indices.assign(sym->source_col_indices, sym->source_col_indices + nnzA);
+
+  // refactorization unit and shared-memory slot
+  {
+    const char* e = std::getenv("B200LU_BATCH_UNIT");
+    const int u = e ? std::atoi(e) : 8;
+    h->unit = (u == 8 || u == 16 || u == 32) ? u : 8;
+    h->units = h->padded / h->unit;
+  }
+
+  ST_TRY(dev_upload(h, &h->d_row_ptr, S.row_ptr));
+  ST_TRY(dev_upload(h, &h->d_col, S.col));
+  ST_TRY(dev_upload(h, &h->d_diag, S.diag));
+  ST_TRY(dev_upload(h, &h->d_trivial_rows, S.trivial_rows));
+  ST_TRY(dev_upload(h, &h->d_pair_row_ptr, S.pair_row_ptr));
+  ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
+  ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
+  {
+    std::vector<FactorMeta> meta;
+    meta.reserve(n);
+    for (int32_t i : S.lower_order) {  // dependency-level order; rows without pivots are final after the scatter
+      if (S.diag[i] > S.row_ptr[i]) meta.push_back(FactorMeta{i, S.row_ptr[i], S.diag[i], S.row_ptr[i + 1]});
+    }
+    h->n_factor_rows = static_cast<int32_t>(meta.size());
+    ST_TRY(dev_upload(h, &h->d_factor_meta, meta));
+  }
+  {
+    std::vector<int32_t> src_of_slot(nnzF, -1);
+    for (int64_t k = 0; k < nnzA; ++k) {
+      const int64_t s = sym->scatter_map[k];
+      if (s < 0 || s >= nnzF || src_of_slot[s] != -1) {
+        h->last_error = "scatter_map is not an injection into the combined pattern";
+        return B200LU_INVALID_ARGUMENT;
+      }
+      src_of_slot[s] = static_cast<int32_t>(k);
+    }
+    ST_TRY(dev_upload(h, &h->d_src_of_slot, src_of_slot));
+    bool need_scale = h->has_match;
+    for (int64_t k = 0; k < nnzA && !need_scale; ++k) need_scale = sym->scatter_scale[k] != 1.0;
+    if (need_scale) {  // off the matching path every scale is exactly 1.0 (src/symbolic.cpp:187): skipped
+      ST_TRY(dev_upload(h, &h->d_scatter_scale, std::vector<double>(sym->scatter_scale, sym->scatter_scale + nnzA)));
+    }
+  }
+  {
+    std::vector<int32_t> p(n), pq(n);
+    for (int64_t i = 0; i < n; ++i) p[i] = static_cast<int32_t>(sym->amd_forward[i]);
+    for (int64_t j = 0; j < n; ++j) pq[j] = h->has_match ? p[sym->col_perm_forward[j]] : p[j];
+    ST_TRY(dev_upload(h, &h->d_p, p));
+    ST_TRY(dev_upload(h, &h->d_pq, pq));
+    if (h->has_match) {
+      ST_TRY(dev_upload(h, &h->d_row_scale, std::vector<double>(sym->row_scale, sym->row_scale + n)));
+      ST_TRY(dev_upload(h, &h->d_col_scale, std::vector<double>(sym->col_scale, sym->col_scale + n)));
+    }
+  }
+  {
+    std::vector<int32_t> arp(n + 1), ac(nnzA);
+    for (int64_t i = 0; i <= n; ++i) arp[i] = static_cast<int32_t>(sym->source_row_offsets[i]);
+    for (int64_t k = 0; k < nnzA; ++k) ac[k] = static_cast<int32_t>(sym->source_col_indices[k]);
+    ST_TRY(dev_upload(h, &h->d_a_row_ptr, arp));
+    ST_TRY(dev_upload(h, &h->d_a_col, ac));
+  }
+  const size_t P = static_cast<size_t>(h->padded);
+  ST_TRY(dev_alloc(h, &h->d_a_int, static_cast<size_t>(nnzA) * P));
+  ST_TRY(dev_alloc(h, &h->d_values, static_cast<size_t>(nnzF) * P));
+  {
+    std::vector<int32_t> flags(static_cast<size_t>(n) * h->units, 0);
+    for (int32_t i : S.trivial_rows) {
+      for (int32_t u = 0; u < h->units; ++u) flags[static_cast<size_t>(i) * h->units + u] = INT_MAX;
+    }
+    ST_TRY(dev_upload(h, &h->d_flags, flags));
+  }
+  ST_TRY(dev_alloc(h, &h->d_failed, 2 * P));
+  ST_TRY(dev_alloc(h, &h->d_tickets, 4));
+  ST_TRY(dev_alloc(h, &h->d_stage_a, static_cast<size_t>(nnzA) * h->batch));
+  for (double** p : {&h->d_stage_in, &h->d_stage_in2, &h->d_stage_out}) ST_TRY(dev_alloc(h, p, static_cast<size_t>(n) * h->batch));
+  ST_TRY(dev_alloc(h, &h->d_gather, static_cast<size_t>(std::max(nnzF, n))));
+  for (double** p : {&h->d_w, &h->d_t1, &h->d_t2, &h->d_b, &h->d_x0, &h->d_x, &h->d_r, &h->d_wv, &h->d_cand, &h->d_best}) {
+    ST_TRY(dev_alloc(h, p, static_cast<size_t>(n) * P));
+  }
+  ST_TRY(dev_alloc(h, &h->d_V, static_cast<size_t>(h->refine_capacity + 1) * std::max<size_t>(n * P, 1)));
+  ST_TRY(dev_alloc(h, &h->d_Z, static_cast<size_t>(h->refine_capacity) * std::max<size_t>(n * P, 1)));
+  const int scal_slots = kSlotCoef + h->refine_capacity + 2;
+  ST_TRY(dev_alloc(h, &h->d_scal, static_cast<size_t>(std::max(scal_slots, kScalSlots)) * P));
+  ST_TRY(dev_alloc(h, &h->d_up, static_cast<size_t>(kUpSlots) * P));
+  ST_TRY(dev_alloc(h, &h->d_partials, static_cast<size_t>(h->groups) * 2 * kBatchParts * 32));
+  CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_scal), static_cast<size_t>(std::max(scal_slots, kScalSlots)) * P * sizeof(double)));
+  CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_up), static_cast<size_t>(kUpSlots) * P * sizeof(double)));
+  CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_failed), 2 * P * sizeof(int32_t)));
+
+  h->dest16 = S.max_row_len <= 65535;
+  ST_TRY(dev_alloc(h, reinterpret_cast<char**>(&h->d_dest), static_cast<size_t>(S.update_pairs) * (h->dest16 ? 2 : 4) + 16));
+  if (n > 0 && S.update_pairs > 0) {
+    const int blocks = std::min<int64_t>(blocks_for(n * 32, 256), 148 * 32);
+    if (h->dest16) {
+      build_dest_kernel<uint16_t><<<blocks, 256, 0, h->stream>>>(static_cast<int32_t>(n), h->d_row_ptr, h->d_col, h->d_diag,
+                                                                 h->d_pair_row_ptr, static_cast<uint16_t*>(h->d_dest));
+    } else {
+      build_dest_kernel<uint32_t><<<blocks, 256, 0, h->stream>>>(static_cast<int32_t>(n), h->d_row_ptr, h->d_col, h->d_diag,
+                                                                 h->d_pair_row_ptr, static_cast<uint32_t*>(h->d_dest));
+    }
+    ST_TRY(check_launch(h, "build_dest_kernel"));
+  }
+
+  // launch geometry: persistent grids sized to what is co-resident
+  cudaDeviceProp prop;
+  CU_TRY(h, cudaGetDeviceProperties(&prop, h->device));
+  {
+    using Fn = void (*)(BFactorArgs);
+    Fn fn = nullptr;
+    if (h->dest16) {
+      fn = h->unit == 8 ? bfactor_kernel<uint16_t, 8, kBWarps> : h->unit == 16 ? bfactor_kernel<uint16_t, 16, kBWarps>
+                                                                                : bfactor_kernel<uint16_t, 32, kBWarps>;
+    } else {
+      fn = h->unit == 8 ? bfactor_kernel<uint32_t, 8, kBWarps> : h->unit == 16 ? bfactor_kernel<uint32_t, 16, kBWarps>
+                                                                                : bfactor_kernel<uint32_t, 32, kBWarps>;
+    }
+    h->factor_fn = fn;
+    // slot: bytes per warp; default 24 KB (one CTA of 8 warps per SM); B200LU_BATCH_SLOT_KB overrides
+    const char* e = std::getenv("B200LU_BATCH_SLOT_KB");
+    int slot_kb = e ? std::atoi(e) : 24;
+    slot_kb = std::max(1, std::min(slot_kb, 27));
+    h->slot_entries = slot_kb * 1024 / (h->unit * 8);
+    h->slot_entries = static_cast<int32_t>(std::min<int64_t>(h->slot_entries, std::max<int64_t>(S.max_row_len, 1)));
+    h->factor_smem = static_cast<size_t>(kBWarps) * h->slot_entries * h->unit * sizeof(double);
+    CU_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->factor_smem)));
+    int occ = 0;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBWarps * 32, h->factor_smem));
+    if (occ < 1) {
+      h->last_error = "batched factor kernel does not fit on an SM";
+      return B200LU_CUDA_ERROR;
+    }
+    h->factor_grid = prop.multiProcessorCount * occ;
+  }
+  {
+    int o1 = 0, o2 = 0;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, btri_kernel<false>, 256, 0));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, btri_kernel<true>, 256, 0));
+    h->tri_grid = prop.multiProcessorCount * std::max(1, std::min(o1, o2));
+  }
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  h->last_error.clear();
+  return B200LU_OK;
+}
+
+void b200lu_batch_destroy(b200lu_batch* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_lower_meta,
+                  h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
+                  h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
+                  h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
+                  h->d_x0, h->d_x, h->d_r, h->d_wv, h->d_cand, h->d_best, h->d_V, h->d_Z, h->d_scal, h->d_up, h->d_partials};
+  for (void* p : ptrs) {
+    if (p) cudaFree(p);
+  }
+  for (cudaEvent_t e : h->ev_start) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_stop) cudaEventDestroy(e);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->h_up) cudaFreeHost(h->h_up);
+  if (h->h_failed) cudaFreeHost(h->h_failed);
+  if (h->owns_stream && h->stream) cudaStreamDestroy(h->stream);
+  cudaGetLastError();
+  delete h;
+}
+
+b200lu_status b200lu_batch_check_pattern(const b200lu_batch* h, int64_t n, const int64_t* row_offsets,
+                                         const int64_t* col_indices) {
+  if (!h || !row_offsets || (!col_indices && h->nnz_source)) return B200LU_INVALID_ARGUMENT;
+  if (n != h->n) return B200LU_PATTERN_MISMATCH;
+  if (std::memcmp(row_offsets, h->src_row_offsets.data(), sizeof(int64_t) * (n + 1)) != 0) return B200LU_PATTERN_MISMATCH;
+  if (h->nnz_source && std::memcmp(col_indices, h->src_col_indices.data(), sizeof(int64_t) * h->nnz_source) != 0) {
+    return B200LU_PATTERN_MISMATCH;
+  }
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_reset_values(b200lu_batch* h, const double* a_values, int on_device) {
+  if (!h || (!a_values && h->nnz_source)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  std::fill(h->valid.begin(), h->valid.end(), 0);
+  const double* src = a_values;
+  if (!on_device && h->nnz_source) {
+    CU_TRY(h, cudaMemcpyAsync(h->d_stage_a, a_values, static_cast<size_t>(h->nnz_source) * h->batch * sizeof(double),
+                              cudaMemcpyHostToDevice, h->stream));
+    src = h->d_stage_a;
+  }
+  {
+    PhaseScope ps(h, B200LU_PHASE_SCATTER);
+    if (h->nnz_source) {
+      dim3 grid(static_cast<unsigned>((h->nnz_source + 31) / 32), static_cast<unsigned>(h->groups));
+      interleave_kernel<<<grid, 256, 0, h->stream>>>(h->nnz_source, h->batch, src, h->d_a_int);
+      ST_TRY(check_launch(h, "interleave_kernel"));
+    }
+  }
+  return launch_scatter(h);
+}
+
+b200lu_status b200lu_batch_factorize_scattered(b200lu_batch* h, int64_t* failed_rows) {
+  if (!h) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  return launch_factor(h, failed_rows);
+}
+
+b200lu_status b200lu_batch_refactorize(b200lu_batch* h, const double* a_values, int on_device, int64_t* failed_rows) {
+  ST_TRY(b200lu_batch_reset_values(h, a_values, on_device));
+  return launch_factor(h, failed_rows);
+}
+
+b200lu_status b200lu_batch_get_values(b200lu_batch* h, int64_t scenario, double* host_out) {
+  if (!h || scenario < 0 || scenario >= h->batch || (!host_out && h->nnz_factors)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->nnz_factors) {
+    bgather_scenario_kernel<<<blocks_for(h->nnz_factors, 256), 256, 0, h->stream>>>(
+        h->nnz_factors, (scenario / 32) * h->nnz_factors, static_cast<int>(scenario % 32), h->d_values, h->d_gather);
+    ST_TRY(check_launch(h, "bgather_scenario_kernel"));
+    CU_TRY(h, cudaMemcpyAsync(host_out, h->d_gather, static_cast<size_t>(h->nnz_factors) * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+  }
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  return B200LU_OK;
+}
+
+int b200lu_batch_valid(const b200lu_batch* h, int64_t scenario) {
+  return h && scenario >= 0 && scenario < h->batch && h->valid[scenario] ? 1 : 0;
+}
+
+static b200lu_status sweep_common(b200lu_batch* h, const double* y, double* x, int on_device, int64_t* failed_rows,
+                                  int which /*0 lower, 1 upper, 2 solve_system*/) {
+  for (int32_t s = 0; h && failed_rows && s < h->batch; ++s) failed_rows[s] = -1;
+  if (!h || (!y && h->n) || (!x && h->n)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  ST_TRY(any_valid(h, which == 0 ? "lower_solve" : which == 1 ? "upper_solve" : "solve_system"));
+  if (h->n == 0) return B200LU_OK;
+  ST_TRY(vec_in(h, y, on_device, h->d_stage_in, h->d_b));
+  if (which == 2) {
+    ST_TRY(solve_int(h, h->d_b, h->d_x));
+  } else {
+    ST_TRY(arm_solve(h));
+    bfill_pending_kernel<<<blocks_for(vec_elems(h), 256), 256, 0, h->stream>>>(vec_elems(h), h->d_x);
+    ST_TRY(check_launch(h, "bfill_pending_kernel"));
+    ST_TRY(which == 0 ? launch_lower(h, h->d_b, h->d_x) : launch_upper(h, h->d_b, h->d_x));
+  }
+  b200lu_status fail = which == 0 ? B200LU_OK : collect_upper_failure(h, failed_rows);
+  ST_TRY(vec_out(h, h->d_x, x, on_device));
+  return fail;
+}
+
+b200lu_status b200lu_batch_lower_solve(b200lu_batch* h, const double* y, double* x, int on_device) {
+  return sweep_common(h, y, x, on_device, nullptr, 0);
+}
+
+b200lu_status b200lu_batch_upper_solve(b200lu_batch* h, const double* y, double* x, int on_device, int64_t* failed_rows) {
+  return sweep_common(h, y, x, on_device, failed_rows, 1);
+}
+
+b200lu_status b200lu_batch_solve(b200lu_batch* h, const double* b, double* x, int on_device, int64_t* failed_rows) {
+  return sweep_common(h, b, x, on_device, failed_rows, 2);
+}
+
+b200lu_status b200lu_batch_relative_residual(b200lu_batch* h, const double* x, const double* b, int on_device,
+                                             double* out) {
+  if (!h || !out || (!x && h->n) || (!b && h->n)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->n == 0) {
+    for (int32_t s = 0; s < h->batch; ++s) out[s] = 0.0;
+    return B200LU_OK;
+  }
+  ST_TRY(vec_in(h, x, on_device, h->d_stage_in, h->d_x));
+  ST_TRY(vec_in(h, b, on_device, h->d_stage_in2, h->d_b));
+  ST_TRY(launch_residual(h, h->d_x, h->d_b, h->d_r, kSlotRes));
+  ST_TRY(read_scalars(h, kSlotRes, 2));
+  for (int32_t s = 0; s < h->batch; ++s) {
+    const double bn = std::sqrt(hscal(h, kSlotBn)[s]);
+    out[s] = std::sqrt(hscal(h, kSlotRes)[s]) / (bn > 0.0 ? bn : 1.0);  // src/sparse.cpp:286-287
+  }
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const double* x0, double* x_out, int on_device,
+                                         int use_preconditioner, const b200lu_refine_config* cfg_in,
+                                         b200lu_refine_outcome* outcomes) {
+  if (!h || !outcomes || (!b && h->n) || (!x0 && h->n) || (!x_out && h->n)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  b200lu_refine_config cfg{20, 1e-14};
+  if (cfg_in) cfg = *cfg_in;
+  if (cfg.max_iterations > h->refine_capacity) {
+    h->last_error = "max_iterations exceeds the handle's refine_capacity";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  if (use_preconditioner) ST_TRY(any_valid(h, "solve_system"));
+  if (h->n) {
+    ST_TRY(vec_in(h, b, on_device, h->d_stage_in, h->d_b));
+    ST_TRY(vec_in(h, x0, on_device, h->d_stage_in2, h->d_x0));
+  }
+  ST_TRY(fgmres_batch(h, h->d_b, h->d_x0, use_preconditioner, cfg, outcomes));
+  if (h->n == 0) return B200LU_OK;
+  return vec_out(h, h->d_best, x_out, on_device);
+}
+
+b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out) {
+  if (!h || !out) return B200LU_INVALID_ARGUMENT;
+  out->batch = h->batch;
+  out->padded_batch = h->padded;
+  out->unit_scenarios = h->unit;
+  out->slot_entries = h->slot_entries;
+  out->staged_rows = 0;
+  out->staged_pairs = 0;
+  for (int64_t i = 0; i < h->n; ++i) {
+    const int64_t len = h->sched.row_ptr[i + 1] - h->sched.row_ptr[i];
+    if (h->sched.diag[i] > h->sched.row_ptr[i] && len <= h->slot_entries) {
+      ++out->staged_rows;
+      out->staged_pairs += h->sched.pair_row_ptr[i + 1] - h->sched.pair_row_ptr[i];
+    }
+  }
+  out->factor_rows = h->n_factor_rows;
+  out->factor_grid = h->factor_grid;
+  out->tri_grid = h->tri_grid;
+  out->n = h->n;
+  out->nnz_factors = h->nnz_factors;
+  out->nnz_source = h->nnz_source;
+  out->update_pairs = h->sched.update_pairs;
+  out->lower_levels = h->sched.lower_levels;
+  out->upper_levels = h->sched.upper_levels;
+  out->device_bytes = h->device_bytes;
+  out->alloc_events = h->alloc_events;
+  out->launches = static_cast<int64_t>(h->launches);
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled) {
+  if (!h) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (enabled && h->ev_start.empty()) {
+    h->ev_start.resize(kMaxTimedLaunches);
+    h->ev_stop.resize(kMaxTimedLaunches);
+    h->ev_phase.assign(kMaxTimedLaunches, 0);
+    for (int i = 0; i < kMaxTimedLaunches; ++i) {
+      CU_TRY(h, cudaEventCreate(&h->ev_start[i]));
+      CU_TRY(h, cudaEventCreate(&h->ev_stop[i]));
+    }
+  }
+  h->timing = enabled != 0;
+  h->ev_used = 0;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset) {
+  if (!h || !ms_out || !count_out) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  for (int p = 0; p < B200LU_NUM_PHASES; ++p) {
+    ms_out[p] = 0.0;
+    count_out[p] = 0;
+  }
+  for (int i = 0; i < h->ev_used; ++i) {
+    float ms = 0.f;
+    CU_TRY(h, cudaEventElapsedTime(&ms, h->ev_start[i], h->ev_stop[i]));
+    ms_out[h->ev_phase[i]] += ms;
+    ++count_out[h->ev_phase[i]];
+  }
+  if (reset) h->ev_used = 0;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_synchronize(b200lu_batch* h) {
+  if (!h) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  return B200LU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,520 @@
+// Scenario batches: B independent systems that share ONE sparsity pattern (same symbolic
+// analysis), factorized and solved together (BASELINE config "batch of 256
+// independent scenario systems").
+//
+// Layout. Every per-scenario array is stored scenario-interleaved in groups of 32:
+//     a[g][k][lane]   = value k of scenario 32*g + lane
+// so a warp that owns (row i, scenarios of group g) reads and writes 256 contiguous bytes per
+// matrix entry, the pattern/index loads are warp-uniform, and the arithmetic of one scenario is
+// exactly the single-system arithmetic of the reference, entry by entry and in the same order:
+// every scenario's L/U values, triangular solves and SpMV are bit-identical to the CPU result.
+// A single system is bound by its dependency chain; in a batch the same chain is
+// shared by 32 scenarios per warp and by all groups at once, which is what makes the path
+// bandwidth-bound.
+#pragma once
+
+#include "common.cuh"
+#include "dest.cuh"
+#include "schedule.hpp"
+
+namespace b200lu {
+
+constexpr int kBatchLanes = 32;
+
+__device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_s32(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// L2-only load (ld.global.cg): values another SM published during this launch.
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------ layout changes
+//
+// src[s][k] (scenario-major, what the caller holds: one CSR value array / one vector per
+// scenario) -> dst[g][k][lane]. Lanes past the last scenario replicate it, so padded lanes run
+// on well-formed data and can never raise a spurious pivot failure. 32x32 tile through shared
+// memory: both sides coalesced.
+__global__ void __launch_bounds__(256)
+interleave_kernel(int64_t len, int32_t batch, const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int32_t g = blockIdx.y;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int s = ty + 8 * j;
+    const int32_t sc = min(g * 32 + s, batch - 1);
+    tile[s][tx] = k0 + tx < len ? src[static_cast<int64_t>(sc) * len + k0 + tx] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int kk = ty + 8 * j;
+    if (k0 + kk < len) dst[(static_cast<int64_t>(g) * len + k0 + kk) * 32 + tx] = tile[tx][kk];
+  }
+}
+
+// dst[s][k] <- src[g][k][lane] for the real scenarios.
+__global__ void __launch_bounds__(256)
+deinterleave_kernel(int64_t len, int32_t batch, const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int32_t g = blockIdx.y;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int kk = ty + 8 * j;
+    tile[kk][tx] = k0 + kk < len ? src[(static_cast<int64_t>(g) * len + k0 + kk) * 32 + tx] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int s = ty + 8 * j;
+    const int32_t sc = g * 32 + s;
+    if (sc < batch && k0 + tx < len) dst[static_cast<int64_t>(sc) * len + k0 + tx] = tile[tx][s];
+  }
+}
+
+// ------------------------------------------------------------------ K1 batched
+//
+// scatter_values (src/numeric.cpp:19-22) for every scenario: gather form through the inverse
+// map, fill slots exactly 0, one coalesced 256-byte store per (slot, group).
+__global__ void __launch_bounds__(256)
+bscatter_kernel(int64_t nnz_factors, int64_t nnz_source, int32_t groups,
+                const int32_t* __restrict__ src_of_slot, const double* __restrict__ a_int,
+                const double* __restrict__ scatter_scale, double* __restrict__ values) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = nnz_factors * groups;
+  for (int64_t t = warp; t < total; t += nwarps) {
+    const int64_t g = t / nnz_factors, s = t - g * nnz_factors;
+    const int32_t k = __ldg(src_of_slot + s);
+    double v = 0.0;
+    if (k >= 0) {
+      v = a_int[(g * nnz_source + k) * 32 + lane];
+      if (scatter_scale != nullptr) v = __dmul_rn(v, __ldg(scatter_scale + k));
+    }
+    values[t * 32 + lane] = v;
+  }
+}
+
+// Pivot check of the rows without a strict-lower entry (elimination leaves them unchanged,
+// src/numeric.cpp:36; the check of src/numeric.cpp:48 still applies).
+__global__ void __launch_bounds__(256)
+btrivial_pivot_kernel(int32_t count, int32_t groups, int64_t nnz_factors, const int32_t* __restrict__ rows,
+                      const int32_t* __restrict__ diag, const double* __restrict__ values, double pivot_floor,
+                      int32_t* failed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(count) * groups) return;
+  const int32_t g = static_cast<int32_t>(warp % groups);
+  const int32_t i = rows[warp / groups];
+  const double v = values[(static_cast<int64_t>(g) * nnz_factors + diag[i]) * 32 + lane];
+  if (fabs(v) <= pivot_floor) atomicMin(failed + g * 32 + lane, i);
+}
+
+// ------------------------------------------------------------------ K2 batched
+//
+// eliminate (src/numeric.cpp:27-58) for S scenarios of one row at a time. A unit of work is
+// (row i, S consecutive scenarios); its warp is laid out as E = 32/S entry lanes x S scenario
+// lanes. Row i of those S scenarios is staged in the warp's shared-memory slot ([entry][S]),
+// the pivots are walked in ascending order exactly as in the reference, and for pivot d the
+// upper entries of row d are streamed from L2/HBM (E entries x S scenarios = 256 bytes per
+// instruction) and applied through the precomputed destination table. Rows longer than the
+// slot are updated in place in global memory (L1-cached: the row is private to the warp until
+// it is published).
+//
+// Dependencies: one generation counter per (row, unit). The owner writes the finished row,
+// fences, and stores the current generation; consumers acquire it before reading the row's
+// upper entries. Units are claimed in (dependency level, unit) order by persistent warps, so a
+// claimed unit's dependencies are finished or owned by a resident warp.
+struct BFactorArgs {
+  int32_t n_rows;        // rows that have pivots, in dependency-level order
+  int32_t units;         // units per row = padded batch / S
+  int32_t slot_entries;  // row entries a warp's shared-memory slot holds
+  int32_t gen;           // generation of this factorization
+  const FactorMeta* meta;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const int32_t* diag;
+  const int64_t* pair_row_ptr;
+  const void* dest;
+  double* values;        // [groups][nnz_factors][32]
+  int64_t nnz_factors;
+  int32_t* flags;        // [n][units]; INT32_MAX for rows without pivots (always ready)
+  double pivot_floor;
+  int32_t* failed;       // [padded batch], atomicMin, INT32_MAX = none
+  unsigned long long* ticket;
+};
+
+template <typename DestT, int S, bool kStaged>
+__device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, double* slot,
+                                             int lane) {
+  constexpr int E = 32 / S;
+  const unsigned full = 0xffffffffu;
+  const int s = lane % S, e = lane / S;
+  const int32_t i = mt.row, lo = mt.lo, nl = mt.dg - mt.lo, len = mt.hi - mt.lo;
+  const int32_t sc0 = u * S;
+  // element (slot k, this lane's scenario) lives at gbase[k * 32]
+  double* gbase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31) + s;
+  double* rowg = gbase + static_cast<int64_t>(lo) * 32;
+  const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
+  double* rs = slot + s;  // staged: entry c of this lane's scenario at rs[c * S]
+
+  auto rd = [&](int32_t c) -> double { return kStaged ? rs[c * S] : rowg[static_cast<int64_t>(c) * 32]; };
+  auto wr = [&](int32_t c, double v) {
+    if (kStaged) rs[c * S] = v; else rowg[static_cast<int64_t>(c) * 32] = v;
+  };
+
+  if (kStaged) {
+    for (int32_t c = e; c < len; c += E) rs[c * S] = rowg[static_cast<int64_t>(c) * 32];
+    if (E > 1) __syncwarp();
+  }
+
+  int64_t p = a.pair_row_ptr[i];
+  for (int32_t k0 = 0; k0 < nl; k0 += 32) {
+    // lane q resolves pivot k0+q: its row d, where d's upper part starts, how long it is, and
+    // whether d is already published (most are: the probe saves the poll round trip later)
+    int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0;
+    if (k0 + lane < nl) {
+      my_d = __ldg(a.col + lo + k0 + lane);
+      my_dd = __ldg(a.diag + my_d);
+      my_m = __ldg(a.row_ptr + my_d + 1) - my_dd - 1;
+      my_ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my_d) * a.units + u) >= a.gen;
+    }
+    __syncwarp();
+    const int32_t cnt = min(32, nl - k0);
+    for (int32_t q = 0; q < cnt; ++q) {
+      const int32_t d = __shfl_sync(full, my_d, q);
+      const int32_t dd = __shfl_sync(full, my_dd, q);
+      const int32_t m = __shfl_sync(full, my_m, q);
+      if (!__shfl_sync(full, my_ready, q)) {
+        const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
+        while (ld_acquire_s32(f) < a.gen) {}
+      }
+      const double* ug = gbase + static_cast<int64_t>(dd) * 32;
+      const double udd = ld_cg(ug);
+      const int32_t k = k0 + q;
+      const double alpha = rd(k) / udd;  // src/numeric.cpp:40
+      int32_t c = e;
+      for (; c + 3 * E < m; c += 4 * E) {
+        double uv[4];
+        int32_t ds[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
+          ds[j] = dest[p + c + j * E];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wr(ds[j], sub_prod(rd(ds[j]), alpha, uv[j]));  // src/numeric.cpp:44
+      }
+      for (; c < m; c += E) {
+        const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
+        const int32_t ds = dest[p + c];
+        wr(ds, sub_prod(rd(ds), alpha, uv));
+      }
+      p += m;
+      if (E > 1) __syncwarp();  // every entry lane has read row[k] and applied its updates
+      // l_id is final (src/numeric.cpp:41): straight to global, nobody reads it during elimination
+      if (e == 0) rowg[static_cast<int64_t>(k) * 32] = alpha;
+    }
+  }
+
+  if (kStaged) {
+    for (int32_t c = nl + e; c < len; c += E) rowg[static_cast<int64_t>(c) * 32] = rs[c * S];
+  }
+  // src/numeric.cpp:48: a failing pivot is recorded (lowest row wins) and the row is published
+  // anyway so dependents never hang (include/rlu/schedule.hpp:29-33, 82-87)
+  if (e == 0 && fabs(rd(nl)) <= a.pivot_floor) atomicMin(a.failed + sc0 + s, i);
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    st_relaxed_s32(a.flags + static_cast<int64_t>(i) * a.units + u, a.gen);
+  }
+}
+
+template <typename DestT, int S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+bfactor_kernel(const BFactorArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  double* slot = smem + static_cast<size_t>(w) * a.slot_entries * S;
+  const unsigned long long total = static_cast<unsigned long long>(a.n_rows) * a.units;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= total) break;
+    const int32_t r = static_cast<int32_t>(t / a.units);
+    const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.units);
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
+    const FactorMeta mt{m4.x, m4.y, m4.z, m4.w};
+    if (mt.hi - mt.lo <= a.slot_entries) {
+      bfactor_unit<DestT, S, true>(a, mt, u, slot, lane);
+    } else {
+      bfactor_unit<DestT, S, false>(a, mt, u, slot, lane);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ K3 batched
+//
+// lower_core / upper_core (src/trisolve.cpp:28-68) for 32 scenarios of one row per warp: lane =
+// scenario, the row's entries are folded in ascending column order (the reference's order) by
+// every lane on its own scenario, so each x is bit-identical to the CPU result. x itself is the
+// ready flag (armed with the pending marker, as in the single-system sweeps). Units are claimed
+// in (dependency level, group) order.
+struct BTriArgs {
+  int32_t n;        // rows
+  int32_t groups;
+  const RowMeta* meta;   // level order; beg/end = the row's strict-lower (L) or strict-upper (U) entries
+  const int32_t* col;
+  const int32_t* diag;
+  const double* values;  // [groups][nnz_factors][32]
+  int64_t nnz_factors;
+  const double* y;       // [groups][n][32]
+  double* x;             // [groups][n][32], armed with the pending marker
+  unsigned long long* ticket;
+  int32_t* failed;       // upper: [padded batch] atomicMax, -1 = none
+};
+
+template <bool kUpper>
+__global__ void __launch_bounds__(256)
+btri_kernel(const BTriArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const unsigned long long total = static_cast<unsigned long long>(a.n) * a.groups;
+  constexpr int kChunk = 8;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1ull);
+    t = __shfl_sync(full, t, 0);
+    if (t >= total) break;
+    const int32_t r = static_cast<int32_t>(t / a.groups);
+    const int32_t g = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.groups);
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
+    const int32_t i = m4.x, beg = m4.y, end = m4.z;
+    const double* vg = a.values + static_cast<int64_t>(g) * a.nnz_factors * 32 + lane;
+    double* xg = a.x + static_cast<int64_t>(g) * a.n * 32 + lane;
+    double acc = a.y[(static_cast<int64_t>(g) * a.n + i) * 32 + lane];
+    double dval = 1.0;
+    if (kUpper) dval = vg[static_cast<int64_t>(__ldg(a.diag + i)) * 32];
+    for (int32_t k = beg; k < end; k += kChunk) {
+      double v[kChunk], xv[kChunk];
+      const double* xp[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        v[j] = 0.0;
+        xv[j] = 0.0;
+        xp[j] = xg;
+        if (k + j < end) {
+          v[j] = vg[static_cast<int64_t>(k + j) * 32];
+          xp[j] = xg + static_cast<int64_t>(__ldg(a.col + k + j)) * 32;
+          xv[j] = ld_l2(xp[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        if (k + j < end) {  // warp-uniform
+          unsigned backoff = 0;
+          while (__any_sync(full, is_pending(xv[j]))) {
+            if (backoff) __nanosleep(backoff);
+            backoff = min(backoff + 32u, 256u);
+            if (is_pending(xv[j])) xv[j] = ld_l2(xp[j]);
+          }
+          acc = sub_prod(acc, v[j], xv[j]);  // src/trisolve.cpp:38 / 57
+        }
+      }
+    }
+    if (kUpper) {
+      if (dval == 0.0) atomicMax(a.failed + g * 32 + lane, i);  // src/trisolve.cpp:60-66
+      acc = acc / dval;
+    }
+    publish(xg + static_cast<int64_t>(i) * 32, acc);
+  }
+}
+
+// solve_system prologue (src/trisolve.cpp:98-105) in the interleaved layout:
+// w[g][p(i)][lane] = D_r[i] * b[g][i][lane]; arms the two sweep buffers.
+__global__ void __launch_bounds__(256)
+bpermute_in_kernel(int32_t n, int32_t groups, const int32_t* __restrict__ p, const double* __restrict__ row_scale,
+                   const double* __restrict__ b, double* __restrict__ w, double* __restrict__ t1,
+                   double* __restrict__ t2) {
+  const double pending = __longlong_as_double(static_cast<long long>(kPendingBits));
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n, i = warp - g * n;
+  double v = b[warp * 32 + lane];
+  if (row_scale != nullptr) v = __dmul_rn(row_scale[i], v);
+  w[(g * n + p[i]) * 32 + lane] = v;
+  t1[warp * 32 + lane] = pending;
+  t2[warp * 32 + lane] = pending;
+}
+
+// solve_system epilogue (src/trisolve.cpp:110-118): x[g][j][lane] = D_c[j] * t[g][pq(j)][lane].
+__global__ void __launch_bounds__(256)
+bpermute_out_kernel(int32_t n, int32_t groups, const int32_t* __restrict__ pq, const double* __restrict__ col_scale,
+                    const double* __restrict__ t, double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n, j = warp - g * n;
+  double v = t[(g * n + pq[j]) * 32 + lane];
+  if (col_scale != nullptr) v = __dmul_rn(col_scale[j], v);
+  x[warp * 32 + lane] = v;
+}
+
+__global__ void __launch_bounds__(256)
+bfill_pending_kernel(int64_t count, double* __restrict__ x) {
+  const double pending = __longlong_as_double(static_cast<long long>(kPendingBits));
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) x[i] = pending;
+}
+
+// ------------------------------------------------------------------ K4 batched
+//
+// Per-scenario reductions: the grid is (kBatchParts, groups); warp q of a group walks a
+// contiguous block of rows with lane = scenario, each lane summing its scenario's terms in row
+// order; the per-warp partials are folded in warp order by bfinish_kernel. Fixed geometry ->
+// results are reproducible run to run (same argument as dot_kernel in refine.cuh: the
+// reference's serial sum, src/sparse.cpp:271-275, cannot be reproduced by a parallel one).
+constexpr int kBatchPartBlocks = 64;                       // blocks per group
+constexpr int kBatchParts = kBatchPartBlocks * 8;          // warps (partials) per group
+
+__device__ __forceinline__ void brow_range(int32_t n, int32_t& i0, int32_t& i1) {
+  const int32_t part = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int32_t per = (n + kBatchParts - 1) / kBatchParts;
+  i0 = min(n, part * per);
+  i1 = min(n, i0 + per);
+}
+
+// r = b - A x (spmv, src/sparse.cpp:135-141: left-to-right accumulation per row) with the
+// partial sums of r^2 and b^2 (relative_residual, src/sparse.cpp:283-288).
+__global__ void __launch_bounds__(256)
+bresidual_kernel(int32_t n, int64_t nnz_source, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                 const double* __restrict__ a_int, const double* __restrict__ x, const double* __restrict__ b,
+                 double* __restrict__ r, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.y;
+  int32_t i0, i1;
+  brow_range(n, i0, i1);
+  const double* ag = a_int + g * nnz_source * 32 + lane;
+  const double* xg = x + g * n * 32 + lane;
+  double s0 = 0.0, s1 = 0.0;
+  for (int32_t i = i0; i < i1; ++i) {
+    double acc = 0.0;
+    for (int32_t k = __ldg(row_ptr + i); k < __ldg(row_ptr + i + 1); ++k) {
+      acc = add_prod(acc, ag[static_cast<int64_t>(k) * 32], xg[static_cast<int64_t>(__ldg(col + k)) * 32]);
+    }
+    const double bi = b[(g * n + i) * 32 + lane];
+    const double ri = __dsub_rn(bi, acc);
+    r[(g * n + i) * 32 + lane] = ri;
+    s0 = add_prod(s0, ri, ri);
+    s1 = add_prod(s1, bi, bi);
+  }
+  const int64_t part = blockIdx.x * 8 + (threadIdx.x >> 5);
+  partials[((g * 2 + 0) * kBatchParts + part) * 32 + lane] = s0;
+  partials[((g * 2 + 1) * kBatchParts + part) * 32 + lane] = s1;
+}
+
+// y = A x
+__global__ void __launch_bounds__(256)
+bspmv_kernel(int32_t n, int32_t groups, int64_t nnz_source, const int32_t* __restrict__ row_ptr,
+             const int32_t* __restrict__ col, const double* __restrict__ a_int, const double* __restrict__ x,
+             double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n, i = warp - g * n;
+  const double* ag = a_int + g * nnz_source * 32 + lane;
+  const double* xg = x + g * n * 32 + lane;
+  double acc = 0.0;
+  for (int32_t k = __ldg(row_ptr + i); k < __ldg(row_ptr + i + 1); ++k) {
+    acc = add_prod(acc, ag[static_cast<int64_t>(k) * 32], xg[static_cast<int64_t>(__ldg(col + k)) * 32]);
+  }
+  y[warp * 32 + lane] = acc;
+}
+
+__global__ void __launch_bounds__(256)
+bdot_kernel(int32_t n, const double* __restrict__ u, const double* __restrict__ v, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.y;
+  int32_t i0, i1;
+  brow_range(n, i0, i1);
+  double s0 = 0.0;
+  for (int32_t i = i0; i < i1; ++i) {
+    const int64_t o = (g * n + i) * 32 + lane;
+    s0 = add_prod(s0, u[o], v[o]);
+  }
+  const int64_t part = blockIdx.x * 8 + (threadIdx.x >> 5);
+  partials[((g * 2 + 0) * kBatchParts + part) * 32 + lane] = s0;
+}
+
+// out[q][g*32+lane] = sum over parts, in part order; count = 1 or 2 running sums
+__global__ void __launch_bounds__(32)
+bfinish_kernel(int32_t count, int32_t padded, const double* __restrict__ partials, double* __restrict__ out) {
+  const int lane = threadIdx.x;
+  const int64_t g = blockIdx.x;
+  for (int q = 0; q < count; ++q) {
+    double s = 0.0;
+    for (int part = 0; part < kBatchParts; ++part) s += partials[((g * 2 + q) * kBatchParts + part) * 32 + lane];
+    out[static_cast<int64_t>(q) * padded + g * 32 + lane] = s;
+  }
+}
+
+// One Gram-Schmidt projection step of cgs2_orthonormalize (src/refine.cpp:13-17) per scenario:
+// h = hs[sc]; coef[sc] += h (row 0 only); w -= h * q.
+__global__ void __launch_bounds__(256)
+bproject_out_kernel(int32_t n, int32_t groups, const double* __restrict__ hs, double* __restrict__ coef,
+                    const double* __restrict__ q, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n, i = warp - g * n;
+  const double h = hs[g * 32 + lane];
+  if (i == 0) coef[g * 32 + lane] = __dadd_rn(coef[g * 32 + lane], h);
+  w[warp * 32 + lane] = add_prod(w[warp * 32 + lane], -h, q[warp * 32 + lane]);
+}
+
+// y += alpha[sc] * x (axpy, src/sparse.cpp:279-281)
+__global__ void __launch_bounds__(256)
+baxpy_kernel(int32_t n, int32_t groups, const double* __restrict__ alpha, const double* __restrict__ x,
+             double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n;
+  y[warp * 32 + lane] = add_prod(y[warp * 32 + lane], alpha[g * 32 + lane], x[warp * 32 + lane]);
+}
+
+// out = in / s[sc]
+__global__ void __launch_bounds__(256)
+bdivide_kernel(int32_t n, int32_t groups, const double* __restrict__ s, const double* __restrict__ in,
+               double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n;
+  out[warp * 32 + lane] = in[warp * 32 + lane] / s[g * 32 + lane];
+}
+
+// dst = src where mask[sc] != 0
+__global__ void __launch_bounds__(256)
+bcopy_masked_kernel(int32_t n, int32_t groups, const double* __restrict__ mask, const double* __restrict__ src,
+                    double* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n;
+  if (mask[g * 32 + lane] != 0.0) dst[warp * 32 + lane] = src[warp * 32 + lane];
+}
+
+}  // namespace b200lu

@@ -1,0 +1,182 @@
+"""Parity of the scenario-batch path (b200lu_batch_*, through the C ABI) with the oracle, on the B200.
+
+Every scenario of a batch must reproduce the single-system results of the reference: L/U values,
+lower/upper/solve_system and SpMV-based residual vectors bit-exact; refinement on the residual
+(its dot products are parallel sums on the device), tolerance written in the test.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2306_14337_b200 as rlu
+from paper_2306_14337_b200.batch import BatchedFactors
+from oracle import oraclebridge as ob
+from oracle import refbridge as rb
+from tests.fixtures import dense_fixture, golden_fixture, kkt_fixture
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not rb.available(), reason="oracle/_ref/librlu_ref.so not built")
+
+
+def _scenarios(fx, batch):
+    """[batch, nnz] values and [batch, n] right-hand sides: the fixture's systems, cycled and
+    rescaled so that no two scenarios are identical."""
+    nsys = len(fx.values)
+    vals = np.stack([fx.values[s % nsys] * (1.0 + 0.03125 * (s // nsys)) for s in range(batch)])
+    rhs = np.stack([fx.rhs[s % nsys] * (1.0 - 0.0625 * (s // nsys)) for s in range(batch)])
+    return vals, rhs
+
+
+def _check_batch(fx, batch, refine=True):
+    vals, rhs = _scenarios(fx, batch)
+    f = BatchedFactors(fx.sym, batch)
+    try:
+        f.reset_values(vals)
+        for s in {0, batch - 1}:
+            assert not f.valid(s)
+            assert np.array_equal(f.values(s), fx.oracle.scatter_values(vals[s]))
+        f.factorize_scattered()
+        lus = []
+        for s in range(batch):
+            ref, failed = fx.oracle.factorize(vals[s])
+            assert failed == -1 and f.valid(s)
+            assert np.array_equal(f.values(s), ref), f"L/U values of scenario {s} differ from the oracle"
+            lus.append(ref)
+        lo, up, x = f.lower_solve(rhs), f.upper_solve(rhs), f.solve_system(rhs)
+        for s in range(batch):
+            assert np.array_equal(lo[s], fx.oracle.lower_solve(lus[s], rhs[s]))
+            assert np.array_equal(up[s], fx.oracle.upper_solve(lus[s], rhs[s])[0])
+            assert np.array_equal(x[s], fx.oracle.solve_system(lus[s], rhs[s])[0])
+        rr = f.relative_residual(x, rhs)
+        for s in range(batch):
+            want = fx.oracle_csr(0, vals[s]).relative_residual(x[s], rhs[s])
+            assert abs(rr[s] - want) <= 1e-12 * max(want, 1e-300) + 1e-30, (s, rr[s], want)
+        if refine:
+            xr, outcomes = f.fgmres_refine(rhs, x)
+            for s in range(batch):
+                A = fx.oracle_csr(0, vals[s])
+                x_ref, its_ref, conv_ref, hist_ref = ob.refine(A, rhs[s], x[s], fx.oracle, lus[s])
+                got, ref = A.relative_residual(xr[s], rhs[s]), A.relative_residual(x_ref, rhs[s])
+                # north star: residual at or below the reference's after refinement; both sit at the
+                # rounding floor, where "at or below" is meaningful only up to a few ulps of it
+                assert got <= max(4 * ref, 1e-15), (s, got, ref)
+                assert outcomes[s].iterations == its_ref and outcomes[s].converged == conv_ref
+                assert len(outcomes[s].residual_history) == len(hist_ref)
+                assert outcomes[s].residual_history[0] == pytest.approx(hist_ref[0], rel=1e-9)
+    finally:
+        f.close()
+
+
+@pytest.mark.parametrize("name", ["kkt_small", "kkt_small_mc64", "random_sparse_60", "random_sparse_120_plain"])
+def test_batch_committed_fixtures_bitwise(name):
+    """tests/golden inputs (no reference needed at run time); partial last group (batch 5)."""
+    _check_batch(golden_fixture(name), 5)
+
+
+@needs_ref
+def test_batch_two_groups_partial():
+    _check_batch(kkt_fixture(700, 300, num_systems=4), 40)
+
+
+@needs_ref
+@pytest.mark.parametrize("unit,slot_kb", [(8, 1), (16, 24), (32, 24), (32, 1)])
+def test_batch_unit_and_slot_variants(unit, slot_kb, monkeypatch):
+    """Every unit width, and a tiny slot so that most rows take the in-place path."""
+    monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
+    monkeypatch.setenv("B200LU_BATCH_SLOT_KB", str(slot_kb))
+    fx = kkt_fixture(700, 300, num_systems=4)
+    f = BatchedFactors(fx.sym, 33)
+    info = f.info
+    f.close()
+    assert info["unit_scenarios"] == unit
+    if slot_kb == 1:
+        assert info["staged_rows"] < info["factor_rows"]
+    _check_batch(fx, 33, refine=False)
+
+
+@needs_ref
+def test_batch_mc64_path():
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7)
+
+
+@needs_ref
+def test_batch_zero_pivot_is_per_scenario():
+    # test_numeric.cpp:173-184 inside a batch: scenario 1 is singular, its neighbours are not
+    good = np.array([[4.0, 1, 0], [1, 4, 1], [0, 1, 4]])
+    bad = np.array([[1.0, 1, 0], [1, 1, 1], [0, 1, 1]])
+    fx = dense_fixture(good)
+    ro, ci = fx.ro, fx.ci
+    rows = np.repeat(np.arange(3), np.diff(ro))
+    vals = np.stack([m[rows, ci] for m in (good, bad, 2 * good)])
+    f = BatchedFactors(fx.sym, 3)
+    with pytest.raises(rlu.ZeroPivotError) as ei:
+        f.refactorize(vals)
+    assert ei.value.scenarios == [1] and ei.value.rows[1] == 1 and ei.value.rows[0] == -1 == ei.value.rows[2]
+    assert ei.value.rows[1] == fx.oracle.factorize(vals[1])[1]
+    assert f.valid(0) and not f.valid(1) and f.valid(2)
+    assert np.array_equal(f.values(0), fx.oracle.factorize(vals[0])[0])
+    assert np.array_equal(f.values(2), fx.oracle.factorize(vals[2])[0])
+    # pivot floor (numeric.hpp:14): every pivot of scenario 0 is below a floor of 100
+    g = BatchedFactors(fx.sym, 3, rlu.FactorOptions(pivot_floor=100.0))
+    failed = g.refactorize(vals, raise_on_zero_pivot=False)
+    assert list(failed) == [fx.oracle.factorize(v, 100.0)[1] for v in vals]
+    f.close()
+    g.close()
+
+
+@needs_ref
+def test_batch_errors_and_determinism():
+    fx = kkt_fixture(700, 300, num_systems=2)
+    vals, rhs = _scenarios(fx, 6)
+    f = BatchedFactors(fx.sym, 6)
+    with pytest.raises(rlu.Error):
+        f.solve_system(rhs)  # factors are not valid (src/trisolve.cpp:20)
+    with pytest.raises(rlu.DimensionError):
+        f.refactorize(vals[:, :-1])
+    with pytest.raises(rlu.PatternMismatchError):
+        f.check_pattern(fx.ro, np.roll(fx.ci, 1))
+    f.check_pattern(fx.ro, fx.ci)
+    f.refactorize(vals)
+    with pytest.raises(rlu.DimensionError):
+        f.solve_system(rhs[:, :-1])
+    a0 = f.info["alloc_events"]
+    x1, o1 = f.fgmres_refine(rhs, f.solve_system(rhs))
+    f.refactorize(vals)
+    x2, o2 = f.fgmres_refine(rhs, f.solve_system(rhs))
+    assert np.array_equal(x1, x2) and [o.residual_history for o in o1] == [o.residual_history for o in o2]
+    assert f.info["alloc_events"] == a0  # no device allocation after create (trisolve.hpp:31-33)
+    f.close()
+
+
+@needs_ref
+def test_batch_device_tensors_in_place():
+    import torch
+    fx = kkt_fixture(700, 300, num_systems=3)
+    vals, rhs = _scenarios(fx, 9)
+    f = BatchedFactors(fx.sym, 9)
+    f.refactorize(torch.from_numpy(vals).cuda())
+    x = f.solve_system(torch.from_numpy(rhs).cuda())
+    assert x.is_cuda
+    for s in range(9):
+        ref = fx.oracle.factorize(vals[s])[0]
+        assert np.array_equal(x[s].cpu().numpy(), fx.oracle.solve_system(ref, rhs[s])[0])
+    f.close()
+
+
+@needs_ref
+def test_batch_c1_all_scenarios():
+    """C1-shaped systems (n+m = 9000), 64 scenarios: LU and x bit-exact for a sample, residuals for all."""
+    fx = kkt_fixture(6300, 2700, num_systems=4)
+    vals, rhs = _scenarios(fx, 64)
+    f = BatchedFactors(fx.sym, 64)
+    f.refactorize(vals)
+    x = f.solve_system(rhs)
+    for s in (0, 17, 31, 32, 63):
+        ref = fx.oracle.factorize(vals[s])[0]
+        assert np.array_equal(f.values(s), ref)
+        assert np.array_equal(x[s], fx.oracle.solve_system(ref, rhs[s])[0])
+    xr, outcomes = f.fgmres_refine(rhs, x)
+    final = f.relative_residual(xr, rhs)
+    assert np.all(final <= 1e-14) and all(o.converged for o in outcomes)
+    f.close()
