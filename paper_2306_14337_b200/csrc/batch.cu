@@ -49,9 +49,9 @@ struct b200lu_batch {
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
   int32_t batch = 0, padded = 0, groups = 0;
-  int unit = 8;          // scenarios per refactorization unit (S)
+  int unit = 16;         // scenarios per refactorization unit (S)
   int32_t units = 0;     // padded / unit
-  int32_t slot_entries = 0;
+  int32_t slot_entries = 0, ring_entries = 0;
   bool has_match = false, dest16 = true;
   std::vector<int64_t> src_row_offsets, src_col_indices;
   std::vector<uint8_t> valid;  // per scenario
@@ -82,7 +82,8 @@ struct b200lu_batch {
   int up_used = 0;
 
   void (*factor_fn)(BFactorArgs) = nullptr;
-  int factor_grid = 0, tri_grid = 0;
+  int factor_grid = 0, tri_grid = 0, tri_grid_upper = 0, tri_grid_chain = 0;
+  int32_t upper_chain_rows = 0;  // leading rows of the U level order handled by the chain launch
   size_t factor_smem = 0;
 
   int64_t alloc_events = 0, device_bytes = 0;
@@ -266,6 +267,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
     a.slot_entries = h->slot_entries;
+    a.ring_entries = h->ring_entries;
     a.gen = h->gen;
     a.meta = h->d_factor_meta;
     a.row_ptr = h->d_row_ptr;
@@ -302,6 +304,8 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
 BTriArgs tri_args(H* h, const RowMeta* meta, const double* y, double* x, int ticket_slot) {
   BTriArgs a;
   a.n = static_cast<int32_t>(h->n);
+  a.first = 0;
+  a.count = a.n;
   a.groups = h->groups;
   a.meta = meta;
   a.col = h->d_col;
@@ -323,14 +327,26 @@ b200lu_status arm_solve(H* h) {
 
 b200lu_status launch_lower(H* h, const double* y, double* x) {
   PhaseScope ps(h, B200LU_PHASE_LOWER);
-  btri_kernel<false><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 1));
+  btri_kernel<false, kTriBufferedWide><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 1));
   return check_launch(h, "btri_kernel<lower>");
 }
 
 b200lu_status launch_upper(H* h, const double* y, double* x) {
   PhaseScope ps(h, B200LU_PHASE_UPPER);
-  btri_kernel<true><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_upper_meta, y, x, 2));
-  return check_launch(h, "btri_kernel<upper>");
+  BTriArgs a = tri_args(h, h->d_upper_meta, y, x, 2);
+  if (h->upper_chain_rows > 0) {  // the narrow leading levels: whole rows parked, one CTA per SM
+    a.count = h->upper_chain_rows;
+    btri_kernel<true, kTriBufferedChain><<<h->tri_grid_chain, 256, tri_upper_smem(kTriBufferedChain), h->stream>>>(a);
+    ST_TRY(check_launch(h, "btri_kernel<upper chain>"));
+  }
+  if (h->upper_chain_rows < h->n) {
+    a.first = h->upper_chain_rows;
+    a.count = static_cast<int32_t>(h->n) - h->upper_chain_rows;
+    a.ticket = h->d_tickets + 3;
+    btri_kernel<true, kTriBufferedWide><<<h->tri_grid_upper, 256, tri_upper_smem(kTriBufferedWide), h->stream>>>(a);
+    ST_TRY(check_launch(h, "btri_kernel<upper wide>"));
+  }
+  return B200LU_OK;
 }
 
 // solve_system (src/trisolve.cpp:90-119) on interleaved vectors; does not synchronise
@@ -664,8 +680,8 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   // refactorization unit and shared-memory slot
   {
     const char* e = std::getenv("B200LU_BATCH_UNIT");
-    const int u = e ? std::atoi(e) : 8;
-    h->unit = (u == 8 || u == 16 || u == 32) ? u : 8;
+    const int u = e ? std::atoi(e) : 16;
+    h->unit = (u == 8 || u == 16 || u == 32) ? u : 16;
     h->units = h->padded / h->unit;
   }
 
@@ -776,13 +792,21 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
                                                                                 : bfactor_kernel<uint32_t, 32, kBWarps>;
     }
     h->factor_fn = fn;
-    // slot: bytes per warp; default 24 KB (one CTA of 8 warps per SM); B200LU_BATCH_SLOT_KB overrides
+    // per warp: a shared-memory row slot and a ring for asynchronously copied pivot rows. Measured
+    // at C2 x 256: occupancy beats staging — with large slots only 8 warps fit an SM
+    // and the kernel is latency-bound (54-72 ms), with no staging and 24 warps per SM it runs at the
+    // L2 bandwidth (32 ms). Defaults: 1 KB slot (rows of up to 8 entries), no ring;
+    // B200LU_BATCH_SLOT_KB / B200LU_BATCH_RING_KB select the staged variants.
     const char* e = std::getenv("B200LU_BATCH_SLOT_KB");
-    int slot_kb = e ? std::atoi(e) : 24;
-    slot_kb = std::max(1, std::min(slot_kb, 27));
+    int slot_kb = e ? std::atoi(e) : 1;
+    e = std::getenv("B200LU_BATCH_RING_KB");
+    int ring_kb = e ? std::atoi(e) : 0;
+    ring_kb = std::max(0, std::min(ring_kb, 26));
+    slot_kb = std::max(1, std::min(slot_kb, 27 - ring_kb));
     h->slot_entries = slot_kb * 1024 / (h->unit * 8);
-    h->slot_entries = static_cast<int32_t>(std::min<int64_t>(h->slot_entries, std::max<int64_t>(S.max_row_len, 1)));
-    h->factor_smem = static_cast<size_t>(kBWarps) * h->slot_entries * h->unit * sizeof(double);
+    h->slot_entries = static_cast<int32_t>(std::min<int64_t>(h->slot_entries, std::max<int64_t>(S.max_row_len, 2)));
+    h->ring_entries = ring_kb * 1024 / (h->unit * 8);
+    h->factor_smem = static_cast<size_t>(kBWarps) * (h->slot_entries + h->ring_entries) * h->unit * sizeof(double);
     CU_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->factor_smem)));
     int occ = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBWarps * 32, h->factor_smem));
@@ -793,10 +817,25 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     h->factor_grid = prop.multiProcessorCount * occ;
   }
   {
-    int o1 = 0, o2 = 0;
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, btri_kernel<false>, 256, 0));
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, btri_kernel<true>, 256, 0));
-    h->tri_grid = prop.multiProcessorCount * std::max(1, std::min(o1, o2));
+    int o1 = 0, o2 = 0, o3 = 0;
+    CU_TRY(h, cudaFuncSetAttribute(btri_kernel<true, kTriBufferedWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(tri_upper_smem(kTriBufferedWide))));
+    CU_TRY(h, cudaFuncSetAttribute(btri_kernel<true, kTriBufferedChain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(tri_upper_smem(kTriBufferedChain))));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, btri_kernel<false, kTriBufferedWide>, 256, 0));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, btri_kernel<true, kTriBufferedWide>, 256,
+                                                            tri_upper_smem(kTriBufferedWide)));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, btri_kernel<true, kTriBufferedChain>, 256,
+                                                            tri_upper_smem(kTriBufferedChain)));
+    h->tri_grid = prop.multiProcessorCount * std::max(1, o1);
+    h->tri_grid_upper = prop.multiProcessorCount * std::max(1, o2);
+    h->tri_grid_chain = prop.multiProcessorCount * std::max(1, o3);
+    // chain part of the U sweep: the leading levels up to the first one at least kChainWidth rows wide
+    const char* e = std::getenv("B200LU_BATCH_CHAIN_WIDTH");
+    const int64_t chain_width = e ? std::atoll(e) : 512;
+    int64_t rows = 0;
+    for (size_t l = 0; l < S.upper_width.size() && S.upper_width[l] < chain_width; ++l) rows += S.upper_width[l];
+    h->upper_chain_rows = static_cast<int32_t>(rows);
   }
   CU_TRY(h, cudaStreamSynchronize(h->stream));
   h->last_error.clear();

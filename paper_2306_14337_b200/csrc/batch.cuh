@@ -21,16 +21,23 @@ namespace b200lu {
 
 constexpr int kBatchLanes = 32;
 
+// Flag load. Relaxed at gpu scope (served by L2, no L1 invalidation): the data it guards is read
+// afterwards with L2-only accesses (ld.global.cg / cp.async.cg) that depend on the flag's value,
+// and the producer fences between its data stores and the flag store.
 __device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_relaxed_s32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// L2-only load (ld.global.cg): values another SM published during this launch.
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+// Every access of the refactorization kernel to `values` bypasses L1: a 128-byte line holds more
+// than one unit's scenarios, so a line cached while one unit of a row was processed would go
+// stale when another SM finishes the neighbouring unit. Loads are gpu-scope relaxed (served by
+// L2), stores are L2-only (st.global.cg), the asynchronous copies are cp.async.cg.
+__device__ __forceinline__ double ld_cg(const double* p) { return ld_l2(p); }
+__device__ __forceinline__ void st_cg(double* p, double v) { __stcg(p, v); }
 
 // ------------------------------------------------------------ layout changes
 //
@@ -137,6 +144,7 @@ struct BFactorArgs {
   int32_t n_rows;        // rows that have pivots, in dependency-level order
   int32_t units;         // units per row = padded batch / S
   int32_t slot_entries;  // row entries a warp's shared-memory slot holds
+  int32_t ring_entries;  // entries (S doubles each) of a warp's pivot-row ring
   int32_t gen;           // generation of this factorization
   const FactorMeta* meta;
   const int32_t* row_ptr;
@@ -152,81 +160,225 @@ struct BFactorArgs {
   unsigned long long* ticket;
 };
 
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// waits until at most `pending` of this thread's most recent copy groups are still in flight
+__device__ __forceinline__ void cp_async_wait_pending(int pending) {
+  switch (pending) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
+}
+
+// One unit = (row i, S scenarios). The pivot rows it consumes are streamed by an asynchronous
+// copy pipeline: up to kCopyDepth pivots ahead of the one being applied, the diagonal + upper
+// entries of row d (S scenarios: (m+1) x S doubles) and the matching slice of the destination
+// table are copied global -> shared (cp.async, L2-only for the values) into the warp's ring, so
+// the update loop itself touches shared memory only and a warp keeps several KB in flight
+// instead of a handful of registers. Pivots that are not published yet when the pipeline reaches
+// them, or that do not fit the ring, are read directly once their flag is set.
+constexpr int kCopyDepth = 4;
+
 template <typename DestT, int S, bool kStaged>
 __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, double* slot,
-                                             int lane) {
+                                             double* ring, int lane) {
   constexpr int E = 32 / S;
+  constexpr int kChunks = S / 2;                       // 16-byte chunks per entry
+  constexpr int kDestPad = sizeof(DestT) == 2 ? 2 : 0; // the destination slice is copied from a 4-byte aligned address
   const unsigned full = 0xffffffffu;
   const int s = lane % S, e = lane / S;
   const int32_t i = mt.row, lo = mt.lo, nl = mt.dg - mt.lo, len = mt.hi - mt.lo;
   const int32_t sc0 = u * S;
-  // element (slot k, this lane's scenario) lives at gbase[k * 32]
-  double* gbase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31) + s;
+  const int32_t R = a.ring_entries;
+  // element (slot k, scenario s of this unit) lives at ubase[k * 32 + s]
+  double* ubase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31);
+  double* gbase = ubase + s;
   double* rowg = gbase + static_cast<int64_t>(lo) * 32;
   const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
   double* rs = slot + s;  // staged: entry c of this lane's scenario at rs[c * S]
 
-  auto rd = [&](int32_t c) -> double { return kStaged ? rs[c * S] : rowg[static_cast<int64_t>(c) * 32]; };
+  // own row in place: L2-only as well (measured: letting L1 cache it costs 20 %, the rows of the
+  // resident warps are several times the L1 capacity)
+  constexpr bool kOwnL1 = false;
+  auto rd = [&](int32_t c) -> double {
+    return kStaged ? rs[c * S] : kOwnL1 ? rowg[static_cast<int64_t>(c) * 32] : ld_cg(rowg + static_cast<int64_t>(c) * 32);
+  };
   auto wr = [&](int32_t c, double v) {
-    if (kStaged) rs[c * S] = v; else rowg[static_cast<int64_t>(c) * 32] = v;
+    if (kStaged) rs[c * S] = v; else if (kOwnL1) rowg[static_cast<int64_t>(c) * 32] = v; else st_cg(rowg + static_cast<int64_t>(c) * 32, v);
+  };
+  auto ring_need = [&](int32_t m) -> int32_t {
+    return m + 1 + static_cast<int32_t>((m * sizeof(DestT) + kDestPad + S * 8 - 1) / (S * 8));
   };
 
   if (kStaged) {
-    for (int32_t c = e; c < len; c += E) rs[c * S] = rowg[static_cast<int64_t>(c) * 32];
-    if (E > 1) __syncwarp();
+    for (int32_t c = e; c < len; c += E) rs[c * S] = ld_cg(rowg + static_cast<int64_t>(c) * 32);
   }
+  __syncwarp();
 
-  int64_t p = a.pair_row_ptr[i];
+  int64_t p_base = a.pair_row_ptr[i];
   for (int32_t k0 = 0; k0 < nl; k0 += 32) {
-    // lane q resolves pivot k0+q: its row d, where d's upper part starts, how long it is, and
-    // whether d is already published (most are: the probe saves the poll round trip later)
-    int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0;
+    // lane q resolves pivot k0+q: its row d, where d's upper part starts, how long it is, its
+    // first update pair, and whether d is already published (most are)
+    int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0, my_off = -1, my_seq = 0;
     if (k0 + lane < nl) {
       my_d = __ldg(a.col + lo + k0 + lane);
       my_dd = __ldg(a.diag + my_d);
       my_m = __ldg(a.row_ptr + my_d + 1) - my_dd - 1;
       my_ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my_d) * a.units + u) >= a.gen;
     }
-    __syncwarp();
+    int32_t incl = my_m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(full, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t my_p = p_base + incl - my_m;
+    p_base += __shfl_sync(full, incl, 31);
     const int32_t cnt = min(32, nl - k0);
+    int32_t issued = 0, committed = 0, head = 0;
     for (int32_t q = 0; q < cnt; ++q) {
+      // ---- keep the copy pipeline full
+      while (issued < cnt && issued - q < kCopyDepth) {
+        const int32_t li = issued;
+        const int32_t m_i = __shfl_sync(full, my_m, li);
+        const int32_t need = ring_need(m_i);
+        int32_t off = -1;
+        if (need <= R) {
+          if (!__shfl_sync(full, my_ready, li)) {
+            const int32_t d_i = __shfl_sync(full, my_d, li);
+            if (ld_acquire_s32(a.flags + static_cast<int64_t>(d_i) * a.units + u) < a.gen) break;  // not published yet
+            if (lane == li) my_ready = 1;
+          }
+          int32_t tail = -1;  // ring offset of the oldest region still in use
+          for (int32_t j = q; j < li && tail < 0; ++j) tail = __shfl_sync(full, my_off, j);
+          if (tail < 0) {
+            off = 0;
+          } else if (head >= tail) {
+            if (need <= R - head) off = head; else if (need < tail) off = 0;
+          } else if (need < tail - head) {
+            off = head;
+          }
+          if (off < 0) break;  // no room until older regions are consumed
+          head = off + need;
+          const int32_t dd_i = __shfl_sync(full, my_dd, li);
+          const int64_t p_i = __shfl_sync(full, my_p, li);
+          const double* src = ubase + static_cast<int64_t>(dd_i) * 32;
+          double* dst = ring + static_cast<size_t>(off) * S;
+          for (int32_t t = lane; t < (m_i + 1) * kChunks; t += 32) {
+            const int32_t c = t / kChunks, hq = t - c * kChunks;
+            cp_async_16(dst + c * S + hq * 2, src + static_cast<int64_t>(c) * 32 + hq * 2);
+          }
+          const char* dsrc = reinterpret_cast<const char*>(dest + p_i);
+          const int32_t shift = static_cast<int32_t>(reinterpret_cast<uintptr_t>(dsrc) & 3);
+          const int32_t words = (static_cast<int32_t>(m_i * sizeof(DestT)) + shift + 3) >> 2;
+          uint32_t* ddst = reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(m_i + 1) * S);
+          for (int32_t t = lane; t < words; t += 32) cp_async_4(ddst + t, dsrc - shift + 4 * t);
+          cp_async_commit();
+        }
+        if (lane == li) {
+          my_off = off;
+          my_seq = committed;
+        }
+        if (off >= 0) ++committed;
+        ++issued;
+      }
+      // ---- apply pivot q
       const int32_t d = __shfl_sync(full, my_d, q);
       const int32_t dd = __shfl_sync(full, my_dd, q);
       const int32_t m = __shfl_sync(full, my_m, q);
-      if (!__shfl_sync(full, my_ready, q)) {
-        const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
-        while (ld_acquire_s32(f) < a.gen) {}
+      const int64_t p = __shfl_sync(full, my_p, q);
+      int32_t off = __shfl_sync(full, my_off, q);
+      if (q >= issued) {  // the pipeline stopped at this pivot (not published yet): it is read directly
+        off = -1;
+        issued = q + 1;
       }
-      const double* ug = gbase + static_cast<int64_t>(dd) * 32;
-      const double udd = ld_cg(ug);
       const int32_t k = k0 + q;
-      const double alpha = rd(k) / udd;  // src/numeric.cpp:40
-      int32_t c = e;
-      for (; c + 3 * E < m; c += 4 * E) {
-        double uv[4];
-        int32_t ds[4];
+      double alpha;
+      if (off >= 0) {
+        cp_async_wait_pending(committed - __shfl_sync(full, my_seq, q) - 1);
+        __syncwarp();  // every lane's share of the copy has landed
+        const double* rg = ring + static_cast<size_t>(off) * S + s;
+        const char* dbytes = reinterpret_cast<const char*>(ring + static_cast<size_t>(off + m + 1) * S);
+        const DestT* dl = reinterpret_cast<const DestT*>(dbytes + (reinterpret_cast<uintptr_t>(dest + p) & 3));
+        alpha = rd(k) / rg[0];  // src/numeric.cpp:40
+        // the destinations of one pivot are distinct slots: read a batch, then write it
+        int32_t c = e;
+        for (; c + 3 * E < m; c += 4 * E) {
+          int32_t ds[4];
+          double rv[4], uv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
-          ds[j] = dest[p + c + j * E];
+          for (int j = 0; j < 4; ++j) {
+            ds[j] = dl[c + j * E];
+            uv[j] = rg[(1 + c + j * E) * S];
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rv[j] = rd(ds[j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));  // src/numeric.cpp:44
         }
+        for (; c < m; c += E) {
+          const int32_t ds = dl[c];
+          wr(ds, sub_prod(rd(ds), alpha, rg[(1 + c) * S]));
+        }
+      } else {
+        if (!__shfl_sync(full, my_ready, q)) {
+          const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
+          while (ld_acquire_s32(f) < a.gen) {}
+        }
+        const double* ug = gbase + static_cast<int64_t>(dd) * 32;
+        alpha = rd(k) / ld_cg(ug);
+        int32_t c = e;
+        for (; c + 7 * E < m; c += 8 * E) {
+          double uv[8], rv[8];
+          int32_t ds[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) wr(ds[j], sub_prod(rd(ds[j]), alpha, uv[j]));  // src/numeric.cpp:44
+          for (int j = 0; j < 8; ++j) {
+            uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
+            ds[j] = dest[p + c + j * E];
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rv[j] = rd(ds[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));
+        }
+        for (; c + 1 * E < m; c += 2 * E) {
+          double uv[2], rv[2];
+          int32_t ds[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
+            ds[j] = dest[p + c + j * E];
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) rv[j] = rd(ds[j]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));
+        }
+        for (; c < m; c += E) {
+          const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
+          const int32_t ds = dest[p + c];
+          wr(ds, sub_prod(rd(ds), alpha, uv));
+        }
       }
-      for (; c < m; c += E) {
-        const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
-        const int32_t ds = dest[p + c];
-        wr(ds, sub_prod(rd(ds), alpha, uv));
-      }
-      p += m;
-      if (E > 1) __syncwarp();  // every entry lane has read row[k] and applied its updates
+      __syncwarp();  // every entry lane has read row[k], applied its updates and left the ring region
       // l_id is final (src/numeric.cpp:41): straight to global, nobody reads it during elimination
-      if (e == 0) rowg[static_cast<int64_t>(k) * 32] = alpha;
+      if (e == 0) st_cg(rowg + static_cast<int64_t>(k) * 32, alpha);
     }
   }
 
   if (kStaged) {
-    for (int32_t c = nl + e; c < len; c += E) rowg[static_cast<int64_t>(c) * 32] = rs[c * S];
+    for (int32_t c = nl + e; c < len; c += E) st_cg(rowg + static_cast<int64_t>(c) * 32, rs[c * S]);
   }
   // src/numeric.cpp:48: a failing pivot is recorded (lowest row wins) and the row is published
   // anyway so dependents never hang (include/rlu/schedule.hpp:29-33, 82-87)
@@ -241,10 +393,11 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
 template <typename DestT, int S, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 bfactor_kernel(const BFactorArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  double* slot = smem + static_cast<size_t>(w) * a.slot_entries * S;
+  double* ring = smem + static_cast<size_t>(w) * (a.slot_entries + a.ring_entries) * S;
+  double* slot = ring + static_cast<size_t>(a.ring_entries) * S;
   const unsigned long long total = static_cast<unsigned long long>(a.n_rows) * a.units;
   while (true) {
     unsigned long long t = 0;
@@ -256,9 +409,9 @@ bfactor_kernel(const BFactorArgs a) {
     const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
     const FactorMeta mt{m4.x, m4.y, m4.z, m4.w};
     if (mt.hi - mt.lo <= a.slot_entries) {
-      bfactor_unit<DestT, S, true>(a, mt, u, slot, lane);
+      bfactor_unit<DestT, S, true>(a, mt, u, slot, ring, lane);
     } else {
-      bfactor_unit<DestT, S, false>(a, mt, u, slot, lane);
+      bfactor_unit<DestT, S, false>(a, mt, u, slot, ring, lane);
     }
     __syncwarp();
   }
@@ -272,7 +425,9 @@ bfactor_kernel(const BFactorArgs a) {
 // ready flag (armed with the pending marker, as in the single-system sweeps). Units are claimed
 // in (dependency level, group) order.
 struct BTriArgs {
-  int32_t n;        // rows
+  int32_t n;        // rows of the matrix
+  int32_t first;    // this launch claims positions [first, first + count) of the level order
+  int32_t count;
   int32_t groups;
   const RowMeta* meta;   // level order; beg/end = the row's strict-lower (L) or strict-upper (U) entries
   const int32_t* col;
@@ -285,53 +440,134 @@ struct BTriArgs {
   int32_t* failed;       // upper: [padded batch] atomicMax, -1 = none
 };
 
-template <bool kUpper>
+// U sweep: the dependency a row waits for LONGEST is normally its first entry (column i+1 or
+// close to it is produced last), and the reference's ascending fold needs that term first. To keep
+// the fold order and still have nothing but the subtraction chain behind the last arrival, the
+// products of entries 1..kTriBuffered are computed ahead (each product is rounded on its own, as
+// in src/trisolve.cpp:57) and parked in the warp's shared-memory buffer; when x of entry 0 lands
+// the row costs one multiply and a chain of subtractions fed from shared memory.
+//
+// The U sweep is launched in two parts: the narrow leading levels (the top of the elimination
+// tree: a long chain, a few rows wide, whose rows have the longest upper parts) with a buffer that
+// parks a whole row, one CTA per SM; then the wide remainder with a small buffer and full
+// occupancy.
+constexpr int kTriChunk = 8;
+constexpr int kTriBufferedWide = 32, kTriBufferedChain = 96;
+constexpr size_t tri_upper_smem(int buffered) { return static_cast<size_t>(8) * buffered * 32 * sizeof(double); }
+
+template <bool kUpper, int kTriBuffered>
 __global__ void __launch_bounds__(256)
 btri_kernel(const BTriArgs a) {
+  extern __shared__ __align__(16) double tri_smem[];
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
-  const unsigned long long total = static_cast<unsigned long long>(a.n) * a.groups;
-  constexpr int kChunk = 8;
-  while (true) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1ull);
-    t = __shfl_sync(full, t, 0);
-    if (t >= total) break;
+  const unsigned long long total = static_cast<unsigned long long>(a.count) * a.groups;
+  double* pb = tri_smem + static_cast<size_t>(threadIdx.x >> 5) * kTriBuffered * 32 + lane;  // kUpper only
+  // Static claim order: warp w takes units w, w + W, w + 2W, ... of the (level, group) order. One
+  // atomic ticket per unit on a single L2 word would serialise the sweep (~2.5 ns each, measured
+  // on the single-system sweeps); static order is deadlock-free for the same reason as the ticket
+  // (the whole grid is resident and the owner of the lowest unfinished unit has nothing before it).
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
+  for (unsigned long long t = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       t < total; t += stride) {
     const int32_t r = static_cast<int32_t>(t / a.groups);
     const int32_t g = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.groups);
-    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + a.first + r);
     const int32_t i = m4.x, beg = m4.y, end = m4.z;
     const double* vg = a.values + static_cast<int64_t>(g) * a.nnz_factors * 32 + lane;
     double* xg = a.x + static_cast<int64_t>(g) * a.n * 32 + lane;
     double acc = a.y[(static_cast<int64_t>(g) * a.n + i) * 32 + lane];
     double dval = 1.0;
     if (kUpper) dval = vg[static_cast<int64_t>(__ldg(a.diag + i)) * 32];
-    for (int32_t k = beg; k < end; k += kChunk) {
-      double v[kChunk], xv[kChunk];
-      const double* xp[kChunk];
+
+    // folds entries [k_begin, k_end) into acc in order
+    auto run = [&](int32_t k_begin, int32_t k_end) {
+      for (int32_t k = k_begin; k < k_end; k += kTriChunk) {
+        double v[kTriChunk], xv[kTriChunk];
+        const double* xp[kTriChunk];
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        v[j] = 0.0;
-        xv[j] = 0.0;
-        xp[j] = xg;
-        if (k + j < end) {
-          v[j] = vg[static_cast<int64_t>(k + j) * 32];
-          xp[j] = xg + static_cast<int64_t>(__ldg(a.col + k + j)) * 32;
-          xv[j] = ld_l2(xp[j]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        if (k + j < end) {  // warp-uniform
-          unsigned backoff = 0;
-          while (__any_sync(full, is_pending(xv[j]))) {
-            if (backoff) __nanosleep(backoff);
-            backoff = min(backoff + 32u, 256u);
-            if (is_pending(xv[j])) xv[j] = ld_l2(xp[j]);
+        for (int j = 0; j < kTriChunk; ++j) {
+          v[j] = 0.0;
+          xv[j] = 0.0;
+          xp[j] = xg;
+          if (k + j < k_end) {
+            v[j] = vg[static_cast<int64_t>(k + j) * 32];
+            xp[j] = xg + static_cast<int64_t>(__ldg(a.col + k + j)) * 32;
+            xv[j] = ld_l2(xp[j]);
           }
-          acc = sub_prod(acc, v[j], xv[j]);  // src/trisolve.cpp:38 / 57
+        }
+#pragma unroll
+        for (int j = 0; j < kTriChunk; ++j) {
+          if (k + j < k_end) {  // warp-uniform
+            unsigned backoff = 0;
+            while (__any_sync(full, is_pending(xv[j]))) {
+              if (backoff) __nanosleep(backoff);
+              backoff = min(backoff + 32u, 256u);
+              if (is_pending(xv[j])) xv[j] = ld_l2(xp[j]);
+            }
+            acc = sub_prod(acc, v[j], xv[j]);  // src/trisolve.cpp:38 / 57
+          }
         }
       }
+    };
+    // parks the products of entries [k_begin, k_end) in the shared-memory buffer, walking the row
+    // BACKWARDS: the far columns (long finished) first, the most recent dependencies last, so no
+    // load is issued behind a wait
+    auto park = [&](int32_t k_begin, int32_t k_end) {
+      for (int32_t k = k_begin + ((k_end - k_begin - 1) / kTriChunk) * kTriChunk; k >= k_begin; k -= kTriChunk) {
+        double v[kTriChunk], xv[kTriChunk];
+        const double* xp[kTriChunk];
+#pragma unroll
+        for (int j = 0; j < kTriChunk; ++j) {
+          v[j] = 0.0;
+          xv[j] = 0.0;
+          xp[j] = xg;
+          if (k + j < k_end) {
+            v[j] = vg[static_cast<int64_t>(k + j) * 32];
+            xp[j] = xg + static_cast<int64_t>(__ldg(a.col + k + j)) * 32;
+            xv[j] = ld_l2(xp[j]);
+          }
+        }
+#pragma unroll
+        for (int j = kTriChunk - 1; j >= 0; --j) {
+          if (k + j < k_end) {  // warp-uniform
+            unsigned backoff = 0;
+            while (__any_sync(full, is_pending(xv[j]))) {
+              if (backoff) __nanosleep(backoff);
+              backoff = min(backoff + 32u, 128u);
+              if (is_pending(xv[j])) xv[j] = ld_l2(xp[j]);
+            }
+            pb[static_cast<size_t>(k + j - k_begin) * 32] = __dmul_rn(v[j], xv[j]);
+          }
+        }
+      }
+    };
+
+    if (!kUpper) {
+      run(beg, end);
+    } else if (beg < end) {
+      const double v0 = vg[static_cast<int64_t>(beg) * 32];
+      const double* xp0 = xg + static_cast<int64_t>(__ldg(a.col + beg)) * 32;
+      const int32_t parked_end = min(end, beg + 1 + kTriBuffered);
+      if (parked_end > beg + 1) park(beg + 1, parked_end);
+      double x0 = ld_l2(xp0);
+      while (__any_sync(full, is_pending(x0))) {
+        if (is_pending(x0)) x0 = ld_l2(xp0);
+      }
+      acc = sub_prod(acc, v0, x0);
+      {
+        const int32_t np = parked_end - beg - 1;
+        int32_t j = 0;
+        for (; j + 8 <= np; j += 8) {
+          double pv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pv[q] = pb[static_cast<size_t>(j + q) * 32];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc = __dsub_rn(acc, pv[q]);
+        }
+        for (; j < np; ++j) acc = __dsub_rn(acc, pb[static_cast<size_t>(j) * 32]);
+      }
+      run(parked_end, end);
     }
     if (kUpper) {
       if (dval == 0.0) atomicMax(a.failed + g * 32 + lane, i);  // src/trisolve.cpp:60-66
