@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """Headline benchmark: refactorize + solve (+ FGMRES) per KKT system, systems/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl b200|reference]
 
-One "step" = one KKT system of the generated sequence taken through the hot path exactly as
-cli::solve_sequence does (reference proj/src/cli.cpp:105-135): value scatter, numeric
-refactorization, solve_system, FGMRES refinement. Inputs are the reference's own synthetic
-generator (gen_sequence, proj/src/kkt.cpp:94-207) and its host-side symbolic analysis, produced once
-before the timed region through the reference bridge (input fixture, not the measured path).
+Workloads (BASELINE.json configs):
+  C5 (default)  a batch of independent ACTIVSg2000-shaped scenario systems per GPU (256 by default)
+                that share one pattern and one symbolic analysis; one "step" takes the whole batch
+                through the hot path with the interleaved scenario-batch kernels
+                (b200lu_batch_*): value scatter, numeric refactorization, solve_system, FGMRES
+                refinement — per scenario exactly what cli::solve_sequence does for one system
+                (reference proj/src/cli.cpp:105-135). The same line carries `single_system`: one
+                ACTIVSg10k-shaped system (C3) through the single-system kernels, i.e. the latency
+                of one refactor+solve.
+  C1..C4        one system per step through the single-system kernels.
+
+Inputs are the reference's own synthetic generator (gen_sequence, proj/src/kkt.cpp:94-207) and its
+host-side symbolic analysis, produced once before the timed region through the reference bridge
+(input fixture, not the measured path).
 
   value   device-resident: values and rhs already in HBM, x stays in HBM.
   e2e     same steps through the public API with HOST buffers: values + rhs copied H2D from pinned
           memory and x copied D2H inside the timed region, every step.
   --impl reference   the unmodified reference CPU implementation (oracle/_ref) on this box's cores.
 
-Under torchrun every rank runs the same workload on its own scenario (y_seed = 2 + rank: same
-pattern, different values) — weak scaling with no data-path collective; NCCL/gloo only carries the
-per-rank timings and residuals to rank 0.
+Under torchrun every rank runs the same workload on its own scenarios (same pattern, different
+values) — weak scaling with no data-path collective; NCCL/gloo only carries the per-rank timings,
+residuals and per-system records to rank 0.
 """
 from __future__ import annotations
 
@@ -41,6 +50,7 @@ WORKLOADS = {
     "C3": (166600, 71400, "ACTIVSg10k-shaped KKT, n+m=238000"),
     "C4": (1120000, 480000, "ACTIVSg70k-shaped KKT, n+m=1600000"),
 }
+BATCH_WORKLOAD = "C5"   # scenarios of C2, batched
 METRIC = "systems/sec (refactor+solve+FGMRES per KKT system)"
 UNIT = "systems/s"
 
@@ -53,6 +63,19 @@ def algorithmic_bytes(n, nnz_a, nnz_f, fgmres_iters=1):
     spmv = 12 * nnz_a + 20 * n
     j = fgmres_iters
     fgmres = (j + 2) * spmv + j * solve + 8 * n * (4 * sum(i + 1 for i in range(j)) + 6 * j + 4) if j else 2 * spmv
+    return dict(scatter=scatter, eliminate=eliminate, solve=solve, spmv=spmv, fgmres=fgmres,
+                total=scatter + eliminate + solve + fgmres)
+
+
+def batch_algorithmic_bytes(batch, n, nnz_a, nnz_f, fgmres_iters=1):
+    """per-scenario VALUE traffic of every phase, the int32 index arrays once
+    per phase (they are shared by all scenarios of a launch)."""
+    j = fgmres_iters
+    scatter = batch * (8 * nnz_a + 8 * nnz_f) + 4 * nnz_f
+    eliminate = batch * 16 * nnz_f + 4 * nnz_f + 8 * n
+    solve = batch * (8 * nnz_f + 60 * n) + 4 * nnz_f + 16 * n
+    spmv = batch * (8 * nnz_a + 16 * n) + 4 * nnz_a + 4 * n
+    fgmres = (j + 2) * spmv + j * solve + batch * 8 * n * (4 * sum(i + 1 for i in range(j)) + 6 * j + 4) if j else 2 * spmv
     return dict(scatter=scatter, eliminate=eliminate, solve=solve, spmv=spmv, fgmres=fgmres,
                 total=scatter + eliminate + solve + fgmres)
 
@@ -181,7 +204,8 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def run_b200(args):
+def measure_single(args, workload, steps, with_cpu_baseline):
+    """One system per step through the single-system kernels. Returns the JSON line (rank 0) or None."""
     import torch
     import torch.distributed as dist
 
@@ -189,13 +213,7 @@ def run_b200(args):
     from oracle import refbridge as rb  # input fixtures + CPU baseline arm only
 
     rank, local_rank, world = dist_env()
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device — the b200lu path has no CPU fallback")
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-
-    n, m, desc = WORKLOADS[args.workload]
+    n, m, desc = WORKLOADS[workload]
     # ---- input fixture (untimed): the reference's generator + host-side symbolic analysis
     seq = rb.RefSequence(n, m, y_seed=2 + rank)
     ref_sym = rb.RefSymbolic(seq.matrix(0), use_scaling=False, use_amd=True)
@@ -271,70 +289,246 @@ def run_b200(args):
         f.set_timing(False)
         return sum(per_step), per_step, iters, phases, f.launch_count - launches0, clocks
 
-    total_ms, per_step, iters, phases, launches, clocks = timed(step_resident, args.steps, args.warmup, True)
-    e2e_total_ms, e2e_steps, _, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2), False)
+    total_ms, per_step, iters, phases, launches, clocks = timed(step_resident, steps, args.warmup, True)
+    e2e_total_ms, e2e_steps, _, _, _, _ = timed(step_e2e, steps, max(1, args.warmup // 2), False)
 
     # ---- parity spot check on the last system processed (oracle/reference as the checker only)
-    k_last = (args.steps - 1) % nsys
+    k_last = (steps - 1) % nsys
     x_last, _ = step_resident(k_last)
     relres = seq.matrix(k_last).relative_residual(x_last.cpu().numpy(), seq.rhs(k_last))
-
     st = f.stats
-    # ---- scenario batch (BASELINE config 5): independent C2-shaped scenarios sharing one
-    # pattern, several in flight per GPU; every rank owns its block of scenarios, no data-path collective
-    batch_info = None
-    batch_ms = 0.0
-    if args.batch_scenarios > 0:
-        from paper_2306_14337_b200.batch import ScenarioBatch
-        from paper_2306_14337_b200.sharding import scenario_assignment, gather_records
-        f.close()
-        bn, bm, bdesc = WORKLOADS["C2"]
-        total_scen = args.batch_scenarios * world
-        mine = scenario_assignment(total_scen, world, rank)
-        seqs = [rb.RefSequence(bn, bm, y_seed=2 + sc, num_systems=1) for sc in mine]
-        bsym_ref = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
-        bsym = rlu.SymbolicFactors.from_arrays(bsym_ref.arrays())
-        bro, bci = seqs[0].pattern()
-        bvals = [torch.from_numpy(q.values(0)).cuda() for q in seqs]
-        brhs = [torch.from_numpy(q.rhs(0)).cuda() for q in seqs]
-        bmats = [rlu.CsrMatrix(seqs[0].n, seqs[0].n, bro, bci, v) for v in bvals]
-        batch = ScenarioBatch(bsym, streams=args.streams, device=local_rank)
-        batch.run(bmats[:2 * args.streams], brhs[:2 * args.streams], keep_x=False)  # warm-up (+ pattern guards)
-        batch.run(bmats, brhs, keep_x=False)
+    f.close()
+
+    # ---- max over ranks
+    t = torch.tensor([total_ms, e2e_total_ms, relres], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max, e2e_ms_max, relres_max = (float(v) for v in t.cpu())
+    if rank != 0:
+        return None
+
+    ms_per_step = total_ms_max / steps
+    value = world * steps / (total_ms_max / 1000.0)
+    e2e_value = world * steps / (e2e_ms_max / 1000.0)
+    med_iters = int(statistics.median(iters)) if iters else 0
+    ab = algorithmic_bytes(N, nnz_a, nnz_f, 0 if args.no_refine else max(med_iters, 0))
+    peak, peak_src = measured_peak()
+    fac_ms, fac_n = phases["factor"]
+    fac_avg_ms = fac_ms / max(fac_n, 1)
+    achieved = ab["eliminate"] / (fac_avg_ms * 1e-3) / 1e9 if fac_avg_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(workload, {}).get("factor_kernel_dram_bytes")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": f"{workload}: {desc}; one system per step per GPU: scatter + refactorize + "
+                        f"solve_system{'' if args.no_refine else ' + fgmres_refine(tol=%g)' % args.refine_tol}; "
+                        "10-system mu sequence, gen_sequence defaults, AMD-only analysis (KLU-style path)",
+            "n": N, "nnz": nnz_a, "nnz_factors": nnz_f, "update_pairs": st["update_pairs"],
+            "levels": st["lower_levels"], "scenario_per_rank": "y_seed = 2 + rank, shared pattern",
+            "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); "
+                  "the per-step working set (values + destination table) also exceeds the 126 MB L2",
+            "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks",
+        },
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms_max / steps,
+                "h2d_bytes_per_step": 8 * nnz_a + 8 * N, "d2h_bytes_per_step": 8 * N,
+                "note": "values + rhs from pinned host memory H2D and x D2H inside the timed region, through "
+                        "the public refactorize/solve_system/fgmres_refine calls"},
+        "gpu_launches": launches,
+        "phases_ms_per_step": {p: v[0] / steps for p, v in phases.items()},
+        "launches_per_step": {p: v[1] / steps for p, v in phases.items()},
+        "refine_iters_median": med_iters, "relres_final_max": relres_max,
+        "roofline": {
+            "kernel": "factor_kernel (K2 numeric refactorization)", "bound": "hbm",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
+            "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
+            "bytes_model": "SURVEY 8(d): eliminate = 20*nnz(L+U) + 8*N per system, one system per launch",
+            "whole_step": {"algorithmic_bytes": ab["total"],
+                           "achieved_gbs": ab["total"] / (ms_per_step * 1e-3) / 1e9,
+                           "frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / peak},
+            "second_bound": f"critical path: {st['lower_levels']} dependency levels per sweep x 3 sweeps",
+        },
+    }
+    if world == 1 and with_cpu_baseline:
+        num, policy = calibrate_reference(ref_sym, seq, rb)
+        reps = max(1, args.cpu_reps)
+        tot = 0.0
+        for r in range(reps):
+            o = num.run_system(seq, r % nsys, refine=not args.no_refine, max_iterations=args.refine_maxit,
+                               tolerance=args.refine_tol)
+            tot += o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"]
+        cpu_ms = tot / reps
+        line["cpu_baseline"] = {
+            "value": 1000.0 / cpu_ms, "unit": UNIT, "ms_per_system": cpu_ms, "cores": policy["threads"],
+            "kind": "reference",
+            "sample": f"{reps} systems of the same {workload} sequence through the unmodified reference "
+                      "(oracle/_ref), best ExecMode per phase after one calibration pass of each mode",
+            "calibration": policy}
+    return line
+
+
+def reference_batch_sample(rb, ref_sym, seqs, threads, refine=True, max_iterations=20, tolerance=1e-14):
+    """The reference on a block of independent scenarios: one scenario per host thread, each through
+    reset_values + factorize_scattered + solve_system + fgmres_refine in ExecMode::sequential (the
+    calls release the GIL). Returns (wall seconds, per-scenario outcomes)."""
+    from concurrent.futures import ThreadPoolExecutor
+    nums = [rb.RefNumeric(ref_sym) for _ in range(threads)]
+
+    def work(t):
+        out = []
+        for s in range(t, len(seqs), threads):
+            out.append(nums[t].run_system(seqs[s], 0, refine=refine, max_iterations=max_iterations, tolerance=tolerance))
+        return out
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(work, range(threads)))
+    return time.perf_counter() - t0, [o for r in res for o in r]
+
+
+def reference_batch_best(rb, ref_sym, seqs, threads, refine, max_iterations, tolerance):
+    """Times the reference on the scenarios `seqs` in both of its ways of using all host threads and
+    keeps the faster: (a) one scenario per thread, ExecMode::sequential inside each; (b) one scenario
+    at a time with the best ExecMode per phase (scheduled_parallel elimination on all threads).
+    Returns (systems/s, description, calibration dict, worst relres)."""
+    wall_a, outs_a = reference_batch_sample(rb, ref_sym, seqs, threads, refine, max_iterations, tolerance)
+    num, policy = calibrate_reference(ref_sym, seqs[0], rb)
+    t0 = time.perf_counter()
+    outs_b = [num.run_system(q, 0, refine=refine, max_iterations=max_iterations, tolerance=tolerance)
+              for q in seqs[:max(2, len(seqs) // 4)]]
+    hot_b = sum(o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"] for o in outs_b) / 1000.0
+    wall_b = time.perf_counter() - t0
+    rate_a, rate_b = len(seqs) / wall_a, len(outs_b) / hot_b
+    cal = {"one_scenario_per_thread": {"systems_per_s": rate_a, "scenarios": len(seqs), "threads": threads},
+           "one_at_a_time_best_exec_mode": {"systems_per_s": rate_b, "scenarios": len(outs_b), "policy": policy,
+                                            "wall_s": wall_b}}
+    if rate_a >= rate_b:
+        return rate_a, (f"{len(seqs)} scenarios, one per host thread ({threads} threads, ExecMode::sequential inside "
+                        "each), wall clock over the block"), cal, max(o["relres_final"] for o in outs_a)
+    return rate_b, (f"{len(outs_b)} scenarios one at a time, eliminate "
+                    f"{'scheduled_parallel x' + str(threads) if policy['factor_parallel'] else 'sequential'}, solves "
+                    f"{'scheduled_parallel' if policy['solve_parallel'] else 'sequential'} (best mode per phase), "
+                    "sum of the four phase clocks"), cal, max(o["relres_final"] for o in outs_b)
+
+
+def run_batch(args):
+    """Default workload: a scenario batch per GPU through the interleaved batch kernels."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_14337_b200 as rlu
+    from paper_2306_14337_b200.batch import BatchedFactors
+    from paper_2306_14337_b200.sharding import SystemRecord, gather_records, scenario_assignment
+    from oracle import refbridge as rb  # input fixtures + CPU baseline arm only
+
+    rank, local_rank, world = dist_env()
+    S = args.scenarios
+    n, m, desc = WORKLOADS["C2"]
+    total_scen = S * world
+    mine = scenario_assignment(total_scen, world, rank)
+    # ---- input fixture (untimed): one generated scenario per y_seed, one symbolic analysis
+    seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1) for sc in mine]
+    ref_sym = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
+    sym = rlu.SymbolicFactors.from_arrays(ref_sym.arrays())
+    ro, ci = seqs[0].pattern()
+    N, nnz_a, nnz_f = seqs[0].n, seqs[0].nnz, ref_sym.nnz_factors
+
+    stream = torch.cuda.current_stream()
+    f = BatchedFactors(sym, S, rlu.FactorOptions(device=local_rank, stream=stream.cuda_stream,
+                                                 refine_capacity=args.refine_maxit))
+    f.check_pattern(ro, ci)  # pattern_equal guard, once per pattern (src/numeric.cpp:15-17)
+    cfg = rlu.RefineConfig(args.refine_maxit, args.refine_tol)
+    host_vals = torch.from_numpy(np.stack([q.values(0) for q in seqs])).pin_memory()
+    host_rhs = torch.from_numpy(np.stack([q.rhs(0) for q in seqs])).pin_memory()
+    dev_vals, dev_rhs = host_vals.cuda(), host_rhs.cuda()
+    dev_b = torch.empty_like(dev_rhs)
+    host_x = torch.empty((S, N), dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+
+    def step_resident():
+        f.refactorize(dev_vals)
+        x = f.solve_system(dev_rhs)
+        if args.no_refine:
+            return x, [0] * S
+        xr, outs = f.fgmres_refine(dev_rhs, x, cfg)
+        return xr, [o.iterations for o in outs]
+
+    def step_e2e():
+        f.refactorize(host_vals.numpy())          # H2D of the values inside the call
+        dev_b.copy_(host_rhs, non_blocking=True)  # rhs H2D on the handle's stream
+        x = f.solve_system(dev_b)
+        its = [0] * S
+        if not args.no_refine:
+            x, outs = f.fgmres_refine(dev_b, x, cfg)
+            its = [o.iterations for o in outs]
+        host_x.copy_(x, non_blocking=True)
+        stream.synchronize()
+        return host_x, its
+
+    def timed(step_fn, steps, warmup, sample_clocks):
+        for _ in range(warmup):
+            step_fn()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        recs, _ = batch.run(bmats, brhs, keep_x=False)
         torch.cuda.synchronize()
-        ev1.record()
+        sampler = ClockSampler(local_rank) if sample_clocks else None
+        f.set_timing(True)
+        launches0 = f.info["launches"]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        its = None
+        for s in range(steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the timed pair)
+            ev[s][0].record()
+            _, its = step_fn()
+            ev[s][1].record()
         torch.cuda.synchronize()
-        batch_ms = ev0.elapsed_time(ev1)
-        allrecs = gather_records([type(r)(mine[r.scenario], r.relres_direct, r.relres_final, r.refine_iters, r.failed_row)
-                                  for r in recs], total_scen, device="cuda") if world > 1 else recs
-        batch_info = {"workload": f"C5-style: {total_scen} independent scenarios of C2 ({bdesc}), shared pattern, "
-                                  f"y_seed = 2 + scenario; {args.streams} systems in flight per GPU "
-                                  "(one handle + CUDA stream + host thread each); values and rhs resident in HBM",
-                      "scenarios_per_gpu": len(mine), "streams_per_gpu": args.streams,
-                      "records": None if allrecs is None else {
-                          "worst_relres_final": max(r.relres_final for r in allrecs),
-                          "median_refine_iters": int(statistics.median(r.refine_iters for r in allrecs)),
-                          "failed": sum(1 for r in allrecs if r.failed_row >= 0)}}
-        batch.close()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sampler else None
+        phases = f.phase_times()
+        f.set_timing(False)
+        return sum(a.elapsed_time(b) for a, b in ev), its, phases, f.info["launches"] - launches0, clocks
 
-    # ---- max over ranks
-    t = torch.tensor([total_ms, e2e_total_ms, relres, batch_ms], dtype=torch.float64, device="cuda")
+    total_ms, iters, phases, launches, clocks = timed(step_resident, args.steps, args.warmup, True)
+    e2e_total_ms, _, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2), False)
+
+    # ---- per-system records (the fields of SystemRecord, include/rlu/report.hpp:14-27) and a parity
+    # spot check against the reference (the checker, not the measured path)
+    x_direct = f.solve_system(dev_rhs)
+    direct = f.relative_residual(x_direct, dev_rhs)
+    x_final, its = step_resident()
+    final = f.relative_residual(x_final, dev_rhs)
+    recs = [SystemRecord(mine[s], float(direct[s]), float(final[s]), int(its[s]), -1) for s in range(S)]
+    spot = [0, S - 1]
+    ref_relres = max(seqs[s].matrix(0).relative_residual(x_final[s].cpu().numpy(), seqs[s].rhs(0)) for s in spot)
+    info = f.info
+    f.close()
+    allrecs = gather_records(recs, total_scen, device="cuda")
+
+    t = torch.tensor([total_ms, e2e_total_ms, ref_relres], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max, e2e_ms_max, relres_max, batch_ms_max = (float(v) for v in t.cpu())
+    total_ms_max, e2e_ms_max, relres_max = (float(v) for v in t.cpu())
+
+    single = None
+    if not args.no_single:
+        single = measure_single(args, args.single_workload, min(args.steps * 2, 20), False)
 
     if rank == 0:
         ms_per_step = total_ms_max / args.steps
-        value = world * args.steps / (total_ms_max / 1000.0)
-        e2e_value = world * args.steps / (e2e_ms_max / 1000.0)
+        value = total_scen * args.steps / (total_ms_max / 1000.0)
+        e2e_value = total_scen * args.steps / (e2e_ms_max / 1000.0)
         med_iters = int(statistics.median(iters)) if iters else 0
-        ab = algorithmic_bytes(N, nnz_a, nnz_f, 0 if args.no_refine else max(med_iters, 0))
+        ab = batch_algorithmic_bytes(S, N, nnz_a, nnz_f, 0 if args.no_refine else max(med_iters, 0))
         peak, peak_src = measured_peak()
         fac_ms, fac_n = phases["factor"]
         fac_avg_ms = fac_ms / max(fac_n, 1)
@@ -342,66 +536,143 @@ def run_b200(args):
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.workload, {}).get("factor_kernel_dram_bytes")
+            traffic = json.load(open(tp)).get(f"C5x{S}", {}).get("factor_kernel_dram_bytes")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": f"{args.workload}: {desc}; one system per step per GPU: scatter + refactorize + "
-                            f"solve_system{'' if args.no_refine else ' + fgmres_refine(tol=%g)' % args.refine_tol}; "
-                            "10-system mu sequence, gen_sequence defaults, AMD-only analysis (KLU-style path)",
-                "n": N, "nnz": nnz_a, "nnz_factors": nnz_f, "update_pairs": st["update_pairs"],
-                "levels": st["lower_levels"], "scenario_per_rank": "y_seed = 2 + rank, shared pattern",
-                "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); "
-                      "the per-step working set (values + destination table) also exceeds the 126 MB L2",
+                "workload": f"C5: batch of {S} independent scenario systems per GPU ({total_scen} in total), each "
+                            f"{desc} (C2-shaped), one shared pattern / symbolic analysis, y_seed = 2 + scenario; one "
+                            f"step = the whole batch through scatter + refactorize + solve_system"
+                            f"{'' if args.no_refine else ' + fgmres_refine(tol=%g)' % args.refine_tol} with the "
+                            "interleaved scenario-batch kernels; gen_sequence defaults, AMD-only analysis (KLU-style path)",
+                "scenarios_per_gpu": S, "n": N, "nnz": nnz_a, "nnz_factors": nnz_f,
+                "update_pairs": info["update_pairs"], "levels": info["lower_levels"],
+                "unit_scenarios": info["unit_scenarios"], "device_gb": round(info["device_bytes"] / 1e9, 2),
+                "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); the "
+                      "per-step working set (9 GB of factor values at 256 scenarios) exceeds the 126 MB L2 anyway",
                 "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks",
             },
             "clocks": clocks,
+            "ms_per_system": ms_per_step / S,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms_max / args.steps,
-                    "h2d_bytes_per_step": 8 * nnz_a + 8 * N, "d2h_bytes_per_step": 8 * N,
-                    "note": "values + rhs from pinned host memory H2D and x D2H inside the timed region, through "
-                            "the public refactorize/solve_system/fgmres_refine calls"},
+                    "h2d_bytes_per_step": 8 * S * (nnz_a + N), "d2h_bytes_per_step": 8 * S * N,
+                    "note": "values + rhs of every scenario from pinned host memory H2D and every x D2H inside the "
+                            "timed region, through the public BatchedFactors refactorize/solve_system/fgmres_refine calls"},
             "gpu_launches": launches,
             "phases_ms_per_step": {p: v[0] / args.steps for p, v in phases.items()},
             "launches_per_step": {p: v[1] / args.steps for p, v in phases.items()},
-            "refine_iters_median": med_iters, "relres_final_max": relres_max,
+            "refine_iters_median": med_iters, "relres_final_max_vs_reference_residual": relres_max,
+            "records": None if allrecs is None else {
+                "systems": len(allrecs), "worst_relres_direct": max(r.relres_direct for r in allrecs),
+                "worst_relres_final": max(r.relres_final for r in allrecs),
+                "median_refine_iters": int(statistics.median(r.refine_iters for r in allrecs)),
+                "failed": sum(1 for r in allrecs if r.failed_row >= 0)},
             "roofline": {
-                "kernel": "factor_kernel (K2 numeric refactorization)", "bound": "hbm",
+                "kernel": "bfactor_kernel (K2 numeric refactorization, scenario-batched)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
-                "bytes_model": "SURVEY 8(d): eliminate = 20*nnz(L+U) + 8*N per system, one system per launch",
+                "bytes_model": f"SURVEY 8(d) C5 row: eliminate = {S} scenarios x 16*nnz(L+U) value bytes + one copy of "
+                               "the int32 indices (4*nnz(L+U) + 8*N), all scenarios in one launch",
                 "whole_step": {"algorithmic_bytes": ab["total"],
                                "achieved_gbs": ab["total"] / (ms_per_step * 1e-3) / 1e9,
                                "frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / peak},
-                "second_bound": f"critical path: {st['lower_levels']} dependency levels per sweep x 3 sweeps",
+                "second_bound": f"critical path: {info['lower_levels']} dependency levels per sweep, shared by all "
+                                f"scenarios of the batch",
             },
         }
-        if batch_info is not None:
-            batch_info["ms_total"] = batch_ms_max
-            batch_info["value"] = args.batch_scenarios * world / (batch_ms_max / 1000.0)
-            batch_info["unit"] = UNIT
-            batch_info["ms_per_system"] = batch_ms_max / (args.batch_scenarios)
-            line["batch"] = batch_info
+        if single is not None:
+            line["single_system"] = {k: single[k] for k in ("value", "unit", "ms_per_step", "config", "e2e",
+                                                            "phases_ms_per_step", "refine_iters_median",
+                                                            "relres_final_max", "roofline", "gpu_launches")}
         if world == 1 and not args.no_cpu_baseline:
-            num, policy = calibrate_reference(ref_sym, seq, rb)
-            reps = max(1, args.cpu_reps)
-            tot = 0.0
-            for r in range(reps):
-                o = num.run_system(seq, r % nsys, refine=not args.no_refine, max_iterations=args.refine_maxit,
-                                   tolerance=args.refine_tol)
-                tot += o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"]
-            cpu_ms = tot / reps
+            threads = rb.max_threads()
+            sample = min(S, threads * max(1, args.cpu_reps // 2))
+            rate, how, cal, worst = reference_batch_best(rb, ref_sym, seqs[:sample], threads, not args.no_refine,
+                                                         args.refine_maxit, args.refine_tol)
             line["cpu_baseline"] = {
-                "value": 1000.0 / cpu_ms, "unit": UNIT, "ms_per_system": cpu_ms, "cores": policy["threads"],
-                "kind": "reference",
-                "sample": f"{reps} systems of the same {args.workload} sequence through the unmodified reference "
-                          "(oracle/_ref), best ExecMode per phase after one calibration pass of each mode",
-                "calibration": policy}
+                "value": rate, "unit": UNIT, "ms_per_system": 1000.0 / rate, "cores": threads, "kind": "reference",
+                "sample": f"of the {S} scenarios of rank 0, through the unmodified reference (oracle/_ref): {how}",
+                "calibration": cal, "worst_relres_final": worst}
         print(json.dumps(line))
-    if args.batch_scenarios <= 0:
-        f.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference_batch(args):
+    """--impl reference, workload C5: the reference on blocks of independent scenarios, one per thread."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from oracle import refbridge as rb
+    n, m, desc = WORKLOADS["C2"]
+    threads = rb.max_threads()
+    block = threads  # one bounded sample per step: one scenario per host thread
+    nseq = block * max(1, min(args.steps + args.warmup, 4))
+    seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1) for sc in range(nseq)]
+    ref_sym = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
+    rate0, how0, cal, _ = reference_batch_best(rb, ref_sym, seqs[:block], threads, True, args.refine_maxit, args.refine_tol)
+    per_thread = cal["one_scenario_per_thread"]["systems_per_s"] >= cal["one_at_a_time_best_exec_mode"]["systems_per_s"]
+    num, _policy = calibrate_reference(ref_sym, seqs[0], rb)
+
+    def one_step(lo):
+        """One bounded sample: `block` scenarios in the faster of the two modes; returns (seconds, outcomes)."""
+        if per_thread:
+            return reference_batch_sample(rb, ref_sym, seqs[lo:lo + block], threads, max_iterations=args.refine_maxit,
+                                          tolerance=args.refine_tol)
+        outs = [num.run_system(q, 0, max_iterations=args.refine_maxit, tolerance=args.refine_tol) for q in seqs[lo:lo + block]]
+        return sum(o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"] for o in outs) / 1000.0, outs
+
+    for w in range(args.warmup):
+        one_step(0)
+    tot, worst, phases = 0.0, 0.0, {"scatter_ms": 0.0, "factor_ms": 0.0, "trisolve_ms": 0.0, "refine_ms": 0.0}
+    for s in range(args.steps):
+        wall, outs = one_step((s * block) % nseq)
+        tot += wall
+        worst = max(worst, max(o["relres_final"] for o in outs))
+        for k in phases:
+            phases[k] += sum(o[k] for o in outs) / len(outs)
+    value = args.steps * block / tot
+    sample = (f"each step = {block} of the C5 scenarios (y_seed = 2 + scenario); mode: " +
+              ("one scenario per host thread, ExecMode::sequential inside each, wall clock over the block" if per_thread
+               else "one scenario at a time, best ExecMode per phase, sum of the four phase clocks") +
+              f"; {threads} host threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5: independent scenario systems, each {desc} (C2-shaped), shared pattern; "
+                               "scatter+eliminate+solve_system+fgmres_refine per system (cli.cpp:105-135); reference CPU path",
+                   "scenarios_per_step": block, "n": seqs[0].n, "nnz": seqs[0].nnz, "nnz_factors": ref_sym.nnz_factors,
+                   "analysis": "use_scaling=false,use_amd=true"},
+        "ms_per_system": 1000.0 * tot / (args.steps * block),
+        "phases_ms_per_system_thread": {k: v / args.steps for k, v in phases.items()},
+        "worst_relres_final": worst,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                         "calibration": cal},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, local_rank, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the b200lu path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.workload == BATCH_WORKLOAD:
+        run_batch(args)
+        return
+    line = measure_single(args, args.workload, args.steps, not args.no_cpu_baseline)
+    if line is not None:
+        print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
@@ -409,21 +680,23 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=BATCH_WORKLOAD, choices=sorted(WORKLOADS) + [BATCH_WORKLOAD])
+    ap.add_argument("--scenarios", type=int, default=256, help="C5: scenarios per GPU")
+    ap.add_argument("--single-workload", default="C3", choices=sorted(WORKLOADS),
+                    help="C5: the single-system measurement reported next to the batch")
+    ap.add_argument("--no-single", action="store_true", help="C5: skip the single-system measurement")
     ap.add_argument("--no-refine", action="store_true")
     ap.add_argument("--refine-tol", type=float, default=1e-14)
     ap.add_argument("--refine-maxit", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=5)
-    ap.add_argument("--batch-scenarios", type=int, default=64, help="scenarios per GPU in the batch leg (0 = skip)")
-    ap.add_argument("--streams", type=int, default=8, help="systems in flight per GPU in the batch leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
-        run_reference(args)
+        (run_reference_batch if args.workload == BATCH_WORKLOAD else run_reference)(args)
     else:
         run_b200(args)
 

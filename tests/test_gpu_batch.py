@@ -80,11 +80,14 @@ def test_batch_two_groups_partial():
 
 
 @needs_ref
-@pytest.mark.parametrize("unit,slot_kb", [(8, 1), (16, 24), (32, 24), (32, 1)])
-def test_batch_unit_and_slot_variants(unit, slot_kb, monkeypatch):
-    """Every unit width, and a tiny slot so that most rows take the in-place path."""
+@pytest.mark.parametrize("unit,slot_kb,ring_kb", [(8, 1, 0), (16, 24, 0), (32, 1, 0), (8, 18, 8), (16, 12, 12),
+                                                  (32, 20, 6), (8, 1, 1)])
+def test_batch_unit_slot_and_ring_variants(unit, slot_kb, ring_kb, monkeypatch):
+    """Every unit width; rows staged in shared memory and rows updated in place (tiny slot); pivot
+    rows read directly and through the cp.async ring (including a ring too small for most pivots)."""
     monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
     monkeypatch.setenv("B200LU_BATCH_SLOT_KB", str(slot_kb))
+    monkeypatch.setenv("B200LU_BATCH_RING_KB", str(ring_kb))
     fx = kkt_fixture(700, 300, num_systems=4)
     f = BatchedFactors(fx.sym, 33)
     info = f.info

@@ -1,16 +1,17 @@
 #!/bin/bash
+# GPU box: full GPU test suite, then the default bench line and the reference arm.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3
-python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_batch.json 2> gpurun_out/bench_batch.err; tail -3 gpurun_out/bench_batch.err
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
+python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; tail -3 gpurun_out/bench_c5.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_c5.json 2>> gpurun_out/bench_c5.err
 python - <<'PY'
 import json
-d=json.loads(open("gpurun_out/bench_batch.json").read().strip().splitlines()[-1])
-print("value", d["value"], "ms/step", d["ms_per_step"], "e2e", d["e2e"]["value"])
-print("batch", json.dumps(d.get("batch"))[:900])
-print("clocks", d["clocks"])
+d=json.loads(open("gpurun_out/bench_c5.json").read().strip().splitlines()[-1])
+print("value", d["value"], "ms/step", d["ms_per_step"], "ms/system", d["ms_per_system"], "e2e", d["e2e"]["value"])
+print("phases", d["phases_ms_per_step"]); print("roofline", {k: d["roofline"][k] for k in ("achieved","frac","avg_launch_ms")}, d["roofline"]["whole_step"])
+print("records", d["records"]); print("cpu", {k: d["cpu_baseline"][k] for k in ("value","cores","sample")})
+print("single", d["single_system"]["value"], d["single_system"]["ms_per_step"], d["single_system"]["roofline"]["frac"])
+print("clocks", d["clocks"], "launches", d["gpu_launches"])
+r=json.loads(open("gpurun_out/bench_ref_c5.json").read().strip().splitlines()[-1])
+print("reference arm", r["value"], r["cpu_baseline"]["sample"])
 PY
-for sidx in 2 4 16; do
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline --streams $sidx 2>/dev/null | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1]); b=d['batch']; print('streams', b['streams_per_gpu'], 'batch systems/s', round(b['value'],1), 'ms/system', round(b['ms_per_system'],3))"
-done
