@@ -224,4 +224,103 @@ inline RefineOutcome classic_refine(const NumericFactors& f, const DenseVector& 
   return detail::refine(b200lu_refine_classic, f, b, x0, cfg, preconditioned);  // src/refine.cpp:150-188
 }
 
+// ---------------------------------------------------------------------------------------------
+// Scenario batches (b200lu_batch_*): `batch` systems over one SymbolicView, factorized and solved
+// together. Arrays are scenario-major: values [batch][nnz(A)], vectors [batch][n].
+class BatchedFactors {
+ public:
+  BatchedFactors(const SymbolicView& sym, index_t batch, const FactorOptions& opt = {})
+      : n_(sym.n), nnz_(sym.nnz_factors), nnz_source_(sym.nnz_source), batch_(batch) {
+    b200lu_options o;
+    b200lu_default_options(&o);
+    o.pivot_floor = opt.pivot_floor;
+    o.device = opt.device;
+    o.stream = opt.stream;
+    o.refine_capacity = opt.refine_capacity;
+    b200lu_batch* h = nullptr;
+    const b200lu_status st = b200lu_batch_create(&sym, &o, batch, &h);
+    if (st != B200LU_OK) {
+      const std::string msg = h ? b200lu_batch_last_error(h) : "";
+      b200lu_batch_destroy(h);
+      if (st == B200LU_NO_DEVICE) throw DeviceError("no CUDA device: the b200lu path has no CPU fallback");
+      if (st == B200LU_CUDA_ERROR) throw DeviceError(msg);
+      throw Error("b200lu_batch_create: " + msg);
+    }
+    h_.reset(h, b200lu_batch_destroy);
+  }
+  index_t n() const { return n_; }
+  index_t batch() const { return batch_; }
+  b200lu_batch* handle() const { return h_.get(); }
+  bool valid(index_t scenario) const { return b200lu_batch_valid(h_.get(), scenario) != 0; }
+  std::vector<double> values(index_t scenario) const {
+    std::vector<double> v(static_cast<std::size_t>(nnz_));
+    check(b200lu_batch_get_values(h_.get(), scenario, v.data()), {});
+    return v;
+  }
+  // refactorize (src/numeric.cpp:70-73) per scenario. Throws ZeroPivotError carrying the first
+  // failing scenario's row; failed_rows() then holds every scenario's row (-1 = factorized).
+  void refactorize(const std::vector<double>& values) {
+    if (static_cast<index_t>(values.size()) != batch_ * nnz_source_) throw DimensionError("refactorize: expected batch * nnz(A) values");
+    failed_.assign(static_cast<std::size_t>(batch_), -1);
+    const b200lu_status st = b200lu_batch_refactorize(h_.get(), values.data(), 0, failed_.data());
+    check(st, failed_);
+  }
+  const std::vector<std::int64_t>& failed_rows() const { return failed_; }
+  std::vector<double> solve_system(const std::vector<double>& b) const {  // src/trisolve.cpp:90-119 per scenario
+    if (static_cast<index_t>(b.size()) != batch_ * n_) throw DimensionError("solve_system: expected batch * n values");
+    std::vector<double> x(b.size());
+    std::vector<std::int64_t> failed(static_cast<std::size_t>(batch_), -1);
+    const b200lu_status st = b200lu_batch_solve(h_.get(), b.data(), x.data(), 0, failed.data());
+    check(st, failed);
+    return x;
+  }
+  std::vector<double> relative_residual(const std::vector<double>& x, const std::vector<double>& b) const {
+    std::vector<double> out(static_cast<std::size_t>(batch_));
+    check(b200lu_batch_relative_residual(h_.get(), x.data(), b.data(), 0, out.data()), {});
+    return out;
+  }
+  // fgmres_refine (src/refine.cpp:39-142) per scenario; x of scenario s is out[s].x.
+  std::vector<RefineOutcome> fgmres_refine(const std::vector<double>& b, const std::vector<double>& x0,
+                                           const RefineConfig& cfg = {}, bool preconditioned = true) const {
+    if (static_cast<index_t>(b.size()) != batch_ * n_ || x0.size() != b.size()) throw DimensionError("refine: expected batch * n values");
+    std::vector<double> x(b.size());
+    std::vector<b200lu_refine_outcome> oc(static_cast<std::size_t>(batch_));
+    b200lu_refine_config c{cfg.max_iterations, cfg.tolerance};
+    check(b200lu_batch_refine_fgmres(h_.get(), b.data(), x0.data(), x.data(), 0, preconditioned ? 1 : 0, &c, oc.data()), {});
+    std::vector<RefineOutcome> out(static_cast<std::size_t>(batch_));
+    for (index_t s = 0; s < batch_; ++s) {
+      out[s].x.assign(x.begin() + s * n_, x.begin() + (s + 1) * n_);
+      out[s].iterations = oc[s].iterations;
+      out[s].converged = oc[s].converged != 0;
+      out[s].residual_history.assign(oc[s].residual_history, oc[s].residual_history + oc[s].history_len);
+    }
+    return out;
+  }
+
+ private:
+  void check(b200lu_status st, const std::vector<std::int64_t>& failed) const {
+    if (st == B200LU_OK) return;
+    std::string msg = b200lu_batch_last_error(h_.get());
+    if (msg.empty()) msg = b200lu_status_string(st);
+    std::int64_t row = -1;
+    for (std::int64_t r : failed) {
+      if (r >= 0) {
+        row = r;
+        break;
+      }
+    }
+    switch (st) {
+      case B200LU_ZERO_PIVOT: throw ZeroPivotError(msg, row);
+      case B200LU_PATTERN_MISMATCH: throw PatternMismatchError("matrix pattern differs from the analyzed pattern");
+      case B200LU_DIMENSION: throw DimensionError(msg);
+      case B200LU_CUDA_ERROR:
+      case B200LU_NO_DEVICE: throw DeviceError(msg);
+      default: throw Error(msg);
+    }
+  }
+  std::shared_ptr<b200lu_batch> h_;
+  index_t n_, nnz_, nnz_source_, batch_;
+  std::vector<std::int64_t> failed_;
+};
+
 }  // namespace rlu_b200

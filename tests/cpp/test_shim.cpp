@@ -247,6 +247,46 @@ int main() {
     }
   });
 
+  run("scenario batch: every scenario equals its single-system run, bit for bit", [] {
+    Sym s({{5, 1, 0, 2}, {1, 6, 1, 0}, {0, 1, 7, 1}, {2, 0, 1, 8}});
+    const index_t B = 3, n = s.n;
+    std::vector<double> vals, rhs;
+    std::vector<CsrMatrix> mats;
+    for (index_t sc = 0; sc < B; ++sc) {
+      CsrMatrix A = s.A;
+      for (std::size_t k = 0; k < A.values.size(); ++k) A.values[k] *= 1.0 + 0.125 * static_cast<double>(sc) * ((k % 3) + 1);
+      vals.insert(vals.end(), A.values.begin(), A.values.end());
+      for (index_t i = 0; i < n; ++i) rhs.push_back(1.0 + static_cast<double>(i + sc));
+      mats.push_back(A);
+    }
+    BatchedFactors bf(s.view, B);
+    bf.refactorize(vals);
+    const std::vector<double> x = bf.solve_system(rhs);
+    const auto outs = bf.fgmres_refine(rhs, x);
+    const auto res = bf.relative_residual(x, rhs);
+    for (index_t sc = 0; sc < B; ++sc) {
+      NumericFactors f = factorize(s.view, mats[sc], kStrict);
+      CHECK(bf.valid(sc) && bf.values(sc) == f.values());
+      const DenseVector b(rhs.begin() + sc * n, rhs.begin() + (sc + 1) * n);
+      CHECK(DenseVector(x.begin() + sc * n, x.begin() + (sc + 1) * n) == solve_system(f, b));
+      CHECK(res[sc] <= 1e-14 && outs[sc].converged);
+    }
+    // a singular scenario fails alone (test_numeric.cpp:173-184 inside a batch)
+    Sym z({{1, 1, 0}, {1, 1, 1}, {0, 1, 1}});
+    std::vector<double> zv = z.A.values, good = {4, 1, 1, 4, 1, 1, 4};
+    std::vector<double> both = good;
+    both.insert(both.end(), zv.begin(), zv.end());
+    BatchedFactors bz(z.view, 2);
+    std::int64_t row = -1;
+    try {
+      bz.refactorize(both);
+    } catch (const ZeroPivotError& e) {
+      row = e.row;
+    }
+    CHECK(row == 1 && bz.failed_rows()[0] == -1 && bz.failed_rows()[1] == 1);
+    CHECK(bz.valid(0) && !bz.valid(1));
+  });
+
   std::printf("%s (%d failure%s)\n", failures ? "FAILED" : "all ok", failures, failures == 1 ? "" : "s");
   return failures ? 1 : 0;
 }
