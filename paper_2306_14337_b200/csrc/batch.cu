@@ -49,7 +49,7 @@ struct b200lu_batch {
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
   int32_t batch = 0, padded = 0, groups = 0;
-  int unit = 16;         // scenarios per refactorization unit (S)
+  int unit = 32;         // scenarios per refactorization unit (S)
   int32_t units = 0;     // padded / unit
   int32_t slot_entries = 0, ring_entries = 0;
   bool has_match = false, dest16 = true;
@@ -680,8 +680,8 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   // refactorization unit and shared-memory slot
   {
     const char* e = std::getenv("B200LU_BATCH_UNIT");
-    const int u = e ? std::atoi(e) : 16;
-    h->unit = (u == 8 || u == 16 || u == 32) ? u : 16;
+    const int u = e ? std::atoi(e) : 32;
+    h->unit = (u == 8 || u == 16 || u == 32) ? u : 32;
     h->units = h->padded / h->unit;
   }
 
@@ -765,7 +765,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_failed), 2 * P * sizeof(int32_t)));
 
   h->dest16 = S.max_row_len <= 65535;
-  ST_TRY(dev_alloc(h, reinterpret_cast<char**>(&h->d_dest), static_cast<size_t>(S.update_pairs) * (h->dest16 ? 2 : 4) + 16));
+  ST_TRY(dev_alloc(h, reinterpret_cast<char**>(&h->d_dest), static_cast<size_t>(S.update_pairs) * (h->dest16 ? 2 : 4) + 256));  // slack: chunk copies read whole words
   if (n > 0 && S.update_pairs > 0) {
     const int blocks = std::min<int64_t>(blocks_for(n * 32, 256), 148 * 32);
     if (h->dest16) {
@@ -783,30 +783,24 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   CU_TRY(h, cudaGetDeviceProperties(&prop, h->device));
   {
     using Fn = void (*)(BFactorArgs);
+    // variant = (min CTAs per SM -> register cap, loads in flight per warp); B200LU_BATCH_VARIANT for experiments
+    const char* ev = std::getenv("B200LU_BATCH_VARIANT");
+    const int variant = ev ? std::atoi(ev) : 0;
+#define B200LU_BF(T, S) \
+  (variant == 1 ? bfactor_kernel<T, S, kBWarps, 6, 8> : variant == 2 ? bfactor_kernel<T, S, kBWarps, 6, 4> \
+   : variant == 3 ? bfactor_kernel<T, S, kBWarps, 4, 16> : variant == 4 ? bfactor_kernel<T, S, kBWarps, 8, 4> \
+   : variant == 5 ? bfactor_kernel<T, S, kBWarps, 3, 16> : bfactor_kernel<T, S, kBWarps, 4, 8>)
     Fn fn = nullptr;
     if (h->dest16) {
-      fn = h->unit == 8 ? bfactor_kernel<uint16_t, 8, kBWarps> : h->unit == 16 ? bfactor_kernel<uint16_t, 16, kBWarps>
-                                                                                : bfactor_kernel<uint16_t, 32, kBWarps>;
+      fn = h->unit == 8 ? B200LU_BF(uint16_t, 8) : h->unit == 16 ? B200LU_BF(uint16_t, 16) : B200LU_BF(uint16_t, 32);
     } else {
-      fn = h->unit == 8 ? bfactor_kernel<uint32_t, 8, kBWarps> : h->unit == 16 ? bfactor_kernel<uint32_t, 16, kBWarps>
-                                                                                : bfactor_kernel<uint32_t, 32, kBWarps>;
+      fn = h->unit == 8 ? B200LU_BF(uint32_t, 8) : h->unit == 16 ? B200LU_BF(uint32_t, 16) : B200LU_BF(uint32_t, 32);
     }
+#undef B200LU_BF
     h->factor_fn = fn;
-    // per warp: a shared-memory row slot and a ring for asynchronously copied pivot rows. Measured
-    // at C2 x 256: occupancy beats staging — with large slots only 8 warps fit an SM
-    // and the kernel is latency-bound (54-72 ms), with no staging and 24 warps per SM it runs at the
-    // L2 bandwidth (32 ms). Defaults: 1 KB slot (rows of up to 8 entries), no ring;
-    // B200LU_BATCH_SLOT_KB / B200LU_BATCH_RING_KB select the staged variants.
-    const char* e = std::getenv("B200LU_BATCH_SLOT_KB");
-    int slot_kb = e ? std::atoi(e) : 1;
-    e = std::getenv("B200LU_BATCH_RING_KB");
-    int ring_kb = e ? std::atoi(e) : 0;
-    ring_kb = std::max(0, std::min(ring_kb, 26));
-    slot_kb = std::max(1, std::min(slot_kb, 27 - ring_kb));
-    h->slot_entries = slot_kb * 1024 / (h->unit * 8);
-    h->slot_entries = static_cast<int32_t>(std::min<int64_t>(h->slot_entries, std::max<int64_t>(S.max_row_len, 2)));
-    h->ring_entries = ring_kb * 1024 / (h->unit * 8);
-    h->factor_smem = static_cast<size_t>(kBWarps) * (h->slot_entries + h->ring_entries) * h->unit * sizeof(double);
+    h->slot_entries = 0;
+    h->ring_entries = 0;
+    h->factor_smem = 0;
     CU_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->factor_smem)));
     int occ = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBWarps * 32, h->factor_smem));

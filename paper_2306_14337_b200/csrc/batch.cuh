@@ -160,229 +160,87 @@ struct BFactorArgs {
   unsigned long long* ticket;
 };
 
-__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_4(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// waits until at most `pending` of this thread's most recent copy groups are still in flight
-__device__ __forceinline__ void cp_async_wait_pending(int pending) {
-  switch (pending) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-  }
+// a += v performed by L2 (red.global.add.f64, round-to-nearest): fire-and-forget, no load latency
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-// One unit = (row i, S scenarios). The pivot rows it consumes are streamed by an asynchronous
-// copy pipeline: up to kCopyDepth pivots ahead of the one being applied, the diagonal + upper
-// entries of row d (S scenarios: (m+1) x S doubles) and the matching slice of the destination
-// table are copied global -> shared (cp.async, L2-only for the values) into the warp's ring, so
-// the update loop itself touches shared memory only and a warp keeps several KB in flight
-// instead of a handful of registers. Pivots that are not published yet when the pipeline reaches
-// them, or that do not fit the ring, are read directly once their flag is set.
-constexpr int kCopyDepth = 4;
-
-template <typename DestT, int S, bool kStaged>
-__device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, double* slot,
-                                             double* ring, int lane) {
+// One unit = (row i, S scenarios). Row i is updated IN PLACE, and every update
+//     a_ij <- a_ij - alpha * u_dj                                  (src/numeric.cpp:44)
+// is issued as a reduction performed by L2: red.add(a_ij, -(alpha * u_dj)). The product is rounded
+// on its own (__dmul_rn) and IEEE a + (-p) == a - p, so the result is bit-identical to the
+// reference's two-rounding update — but the warp never waits for a_ij: no read-modify-write
+// chain, only the streaming loads of row d's upper entries (8 of them, 2 KB per warp, in flight
+// at once) and one load of a_id per pivot for alpha = a_id / u_dd (src/numeric.cpp:40), which the
+// memory model orders after this thread's own earlier reductions to that address. Per-address
+// order is what bit-exactness needs (pivots ascending per slot): with S = 32 one lane owns one
+// scenario, so all operations on an address come from one thread in program order.
+template <typename DestT, int S, int kUnroll>
+__device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, int lane) {
   constexpr int E = 32 / S;
-  constexpr int kChunks = S / 2;                       // 16-byte chunks per entry
-  constexpr int kDestPad = sizeof(DestT) == 2 ? 2 : 0; // the destination slice is copied from a 4-byte aligned address
   const unsigned full = 0xffffffffu;
   const int s = lane % S, e = lane / S;
-  const int32_t i = mt.row, lo = mt.lo, nl = mt.dg - mt.lo, len = mt.hi - mt.lo;
+  const int32_t i = mt.row, lo = mt.lo, nl = mt.dg - mt.lo;
   const int32_t sc0 = u * S;
-  const int32_t R = a.ring_entries;
-  // element (slot k, scenario s of this unit) lives at ubase[k * 32 + s]
-  double* ubase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31);
-  double* gbase = ubase + s;
+  // element (slot k, scenario s of this unit) lives at gbase[k * 32]
+  double* gbase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31) + s;
   double* rowg = gbase + static_cast<int64_t>(lo) * 32;
   const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
-  double* rs = slot + s;  // staged: entry c of this lane's scenario at rs[c * S]
 
-  // own row in place: L2-only as well (measured: letting L1 cache it costs 20 %, the rows of the
-  // resident warps are several times the L1 capacity)
-  constexpr bool kOwnL1 = false;
-  auto rd = [&](int32_t c) -> double {
-    return kStaged ? rs[c * S] : kOwnL1 ? rowg[static_cast<int64_t>(c) * 32] : ld_cg(rowg + static_cast<int64_t>(c) * 32);
-  };
-  auto wr = [&](int32_t c, double v) {
-    if (kStaged) rs[c * S] = v; else if (kOwnL1) rowg[static_cast<int64_t>(c) * 32] = v; else st_cg(rowg + static_cast<int64_t>(c) * 32, v);
-  };
-  auto ring_need = [&](int32_t m) -> int32_t {
-    return m + 1 + static_cast<int32_t>((m * sizeof(DestT) + kDestPad + S * 8 - 1) / (S * 8));
-  };
-
-  if (kStaged) {
-    for (int32_t c = e; c < len; c += E) rs[c * S] = ld_cg(rowg + static_cast<int64_t>(c) * 32);
-  }
-  __syncwarp();
-
-  int64_t p_base = a.pair_row_ptr[i];
+  int64_t p = a.pair_row_ptr[i];
   for (int32_t k0 = 0; k0 < nl; k0 += 32) {
-    // lane q resolves pivot k0+q: its row d, where d's upper part starts, how long it is, its
-    // first update pair, and whether d is already published (most are)
-    int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0, my_off = -1, my_seq = 0;
+    // lane q resolves pivot k0+q: its row d, where d's upper part starts, how long it is, and
+    // whether d is already published (most are: the probe saves the poll round trip later)
+    int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0;
     if (k0 + lane < nl) {
       my_d = __ldg(a.col + lo + k0 + lane);
       my_dd = __ldg(a.diag + my_d);
       my_m = __ldg(a.row_ptr + my_d + 1) - my_dd - 1;
       my_ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my_d) * a.units + u) >= a.gen;
     }
-    int32_t incl = my_m;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t t = __shfl_up_sync(full, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int64_t my_p = p_base + incl - my_m;
-    p_base += __shfl_sync(full, incl, 31);
+    __syncwarp();
     const int32_t cnt = min(32, nl - k0);
-    int32_t issued = 0, committed = 0, head = 0;
     for (int32_t q = 0; q < cnt; ++q) {
-      // ---- keep the copy pipeline full
-      while (issued < cnt && issued - q < kCopyDepth) {
-        const int32_t li = issued;
-        const int32_t m_i = __shfl_sync(full, my_m, li);
-        const int32_t need = ring_need(m_i);
-        int32_t off = -1;
-        if (need <= R) {
-          if (!__shfl_sync(full, my_ready, li)) {
-            const int32_t d_i = __shfl_sync(full, my_d, li);
-            if (ld_acquire_s32(a.flags + static_cast<int64_t>(d_i) * a.units + u) < a.gen) break;  // not published yet
-            if (lane == li) my_ready = 1;
-          }
-          int32_t tail = -1;  // ring offset of the oldest region still in use
-          for (int32_t j = q; j < li && tail < 0; ++j) tail = __shfl_sync(full, my_off, j);
-          if (tail < 0) {
-            off = 0;
-          } else if (head >= tail) {
-            if (need <= R - head) off = head; else if (need < tail) off = 0;
-          } else if (need < tail - head) {
-            off = head;
-          }
-          if (off < 0) break;  // no room until older regions are consumed
-          head = off + need;
-          const int32_t dd_i = __shfl_sync(full, my_dd, li);
-          const int64_t p_i = __shfl_sync(full, my_p, li);
-          const double* src = ubase + static_cast<int64_t>(dd_i) * 32;
-          double* dst = ring + static_cast<size_t>(off) * S;
-          for (int32_t t = lane; t < (m_i + 1) * kChunks; t += 32) {
-            const int32_t c = t / kChunks, hq = t - c * kChunks;
-            cp_async_16(dst + c * S + hq * 2, src + static_cast<int64_t>(c) * 32 + hq * 2);
-          }
-          const char* dsrc = reinterpret_cast<const char*>(dest + p_i);
-          const int32_t shift = static_cast<int32_t>(reinterpret_cast<uintptr_t>(dsrc) & 3);
-          const int32_t words = (static_cast<int32_t>(m_i * sizeof(DestT)) + shift + 3) >> 2;
-          uint32_t* ddst = reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(m_i + 1) * S);
-          for (int32_t t = lane; t < words; t += 32) cp_async_4(ddst + t, dsrc - shift + 4 * t);
-          cp_async_commit();
-        }
-        if (lane == li) {
-          my_off = off;
-          my_seq = committed;
-        }
-        if (off >= 0) ++committed;
-        ++issued;
-      }
-      // ---- apply pivot q
-      const int32_t d = __shfl_sync(full, my_d, q);
       const int32_t dd = __shfl_sync(full, my_dd, q);
       const int32_t m = __shfl_sync(full, my_m, q);
-      const int64_t p = __shfl_sync(full, my_p, q);
-      int32_t off = __shfl_sync(full, my_off, q);
-      if (q >= issued) {  // the pipeline stopped at this pivot (not published yet): it is read directly
-        off = -1;
-        issued = q + 1;
+      if (!__shfl_sync(full, my_ready, q)) {
+        const int32_t d = __shfl_sync(full, my_d, q);
+        const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
+        while (ld_acquire_s32(f) < a.gen) {}
       }
+      const double* ug = gbase + static_cast<int64_t>(dd) * 32;
       const int32_t k = k0 + q;
-      double alpha;
-      if (off >= 0) {
-        cp_async_wait_pending(committed - __shfl_sync(full, my_seq, q) - 1);
-        __syncwarp();  // every lane's share of the copy has landed
-        const double* rg = ring + static_cast<size_t>(off) * S + s;
-        const char* dbytes = reinterpret_cast<const char*>(ring + static_cast<size_t>(off + m + 1) * S);
-        const DestT* dl = reinterpret_cast<const DestT*>(dbytes + (reinterpret_cast<uintptr_t>(dest + p) & 3));
-        alpha = rd(k) / rg[0];  // src/numeric.cpp:40
-        // the destinations of one pivot are distinct slots: read a batch, then write it
-        int32_t c = e;
-        for (; c + 3 * E < m; c += 4 * E) {
-          int32_t ds[4];
-          double rv[4], uv[4];
+      if (E > 1) __syncwarp();  // the other entry lanes' reductions of the previous pivot are issued
+      const double udd = ld_cg(ug);
+      const double aik = ld_cg(rowg + static_cast<int64_t>(k) * 32);
+      // first batch of row d's upper entries in flight while alpha is being formed
+      const double nalpha = -(aik / udd);  // src/numeric.cpp:40; the sign is exact
+      int32_t c = e;
+      for (; c + (kUnroll - 1) * E < m; c += kUnroll * E) {
+        double uv[kUnroll];
+        int32_t ds[kUnroll];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            ds[j] = dl[c + j * E];
-            uv[j] = rg[(1 + c + j * E) * S];
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) rv[j] = rd(ds[j]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));  // src/numeric.cpp:44
+        for (int j = 0; j < kUnroll; ++j) {
+          uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
+          ds[j] = dest[p + c + j * E];
         }
-        for (; c < m; c += E) {
-          const int32_t ds = dl[c];
-          wr(ds, sub_prod(rd(ds), alpha, rg[(1 + c) * S]));
-        }
-      } else {
-        if (!__shfl_sync(full, my_ready, q)) {
-          const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
-          while (ld_acquire_s32(f) < a.gen) {}
-        }
-        const double* ug = gbase + static_cast<int64_t>(dd) * 32;
-        alpha = rd(k) / ld_cg(ug);
-        int32_t c = e;
-        for (; c + 7 * E < m; c += 8 * E) {
-          double uv[8], rv[8];
-          int32_t ds[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
-            ds[j] = dest[p + c + j * E];
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) rv[j] = rd(ds[j]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));
-        }
-        for (; c + 1 * E < m; c += 2 * E) {
-          double uv[2], rv[2];
-          int32_t ds[2];
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
-            ds[j] = dest[p + c + j * E];
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) rv[j] = rd(ds[j]);
-#pragma unroll
-          for (int j = 0; j < 2; ++j) wr(ds[j], sub_prod(rv[j], alpha, uv[j]));
-        }
-        for (; c < m; c += E) {
-          const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
-          const int32_t ds = dest[p + c];
-          wr(ds, sub_prod(rd(ds), alpha, uv));
-        }
+        for (int j = 0; j < kUnroll; ++j) red_add_f64(rowg + static_cast<int64_t>(ds[j]) * 32, __dmul_rn(nalpha, uv[j]));
       }
-      __syncwarp();  // every entry lane has read row[k], applied its updates and left the ring region
-      // l_id is final (src/numeric.cpp:41): straight to global, nobody reads it during elimination
-      if (e == 0) st_cg(rowg + static_cast<int64_t>(k) * 32, alpha);
+      for (; c < m; c += E) {
+        const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
+        red_add_f64(rowg + static_cast<int64_t>(dest[p + c]) * 32, __dmul_rn(nalpha, uv));
+      }
+      p += m;
+      // l_id is final (src/numeric.cpp:41); nobody reads it during elimination
+      if (e == 0) st_cg(rowg + static_cast<int64_t>(k) * 32, -nalpha);
     }
   }
 
-  if (kStaged) {
-    for (int32_t c = nl + e; c < len; c += E) st_cg(rowg + static_cast<int64_t>(c) * 32, rs[c * S]);
-  }
   // src/numeric.cpp:48: a failing pivot is recorded (lowest row wins) and the row is published
   // anyway so dependents never hang (include/rlu/schedule.hpp:29-33, 82-87)
-  if (e == 0 && fabs(rd(nl)) <= a.pivot_floor) atomicMin(a.failed + sc0 + s, i);
+  __syncwarp();
+  if (e == 0 && fabs(ld_cg(rowg + static_cast<int64_t>(nl) * 32)) <= a.pivot_floor) atomicMin(a.failed + sc0 + s, i);
   __syncwarp();
   if (lane == 0) {
     __threadfence();
@@ -390,14 +248,10 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
   }
 }
 
-template <typename DestT, int S, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+template <typename DestT, int S, int WARPS, int kMinBlocks, int kUnroll>
+__global__ void __launch_bounds__(WARPS * 32, kMinBlocks)
 bfactor_kernel(const BFactorArgs a) {
-  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  double* ring = smem + static_cast<size_t>(w) * (a.slot_entries + a.ring_entries) * S;
-  double* slot = ring + static_cast<size_t>(a.ring_entries) * S;
   const unsigned long long total = static_cast<unsigned long long>(a.n_rows) * a.units;
   while (true) {
     unsigned long long t = 0;
@@ -407,12 +261,7 @@ bfactor_kernel(const BFactorArgs a) {
     const int32_t r = static_cast<int32_t>(t / a.units);
     const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.units);
     const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
-    const FactorMeta mt{m4.x, m4.y, m4.z, m4.w};
-    if (mt.hi - mt.lo <= a.slot_entries) {
-      bfactor_unit<DestT, S, true>(a, mt, u, slot, ring, lane);
-    } else {
-      bfactor_unit<DestT, S, false>(a, mt, u, slot, ring, lane);
-    }
+    bfactor_unit<DestT, S, kUnroll>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, u, lane);
     __syncwarp();
   }
 }

@@ -80,22 +80,30 @@ def test_batch_two_groups_partial():
 
 
 @needs_ref
-@pytest.mark.parametrize("unit,slot_kb,ring_kb", [(8, 1, 0), (16, 24, 0), (32, 1, 0), (8, 18, 8), (16, 12, 12),
-                                                  (32, 20, 6), (8, 1, 1)])
-def test_batch_unit_slot_and_ring_variants(unit, slot_kb, ring_kb, monkeypatch):
-    """Every unit width; rows staged in shared memory and rows updated in place (tiny slot); pivot
-    rows read directly and through the cp.async ring (including a ring too small for most pivots)."""
+@pytest.mark.parametrize("unit", [8, 16, 32])
+def test_batch_unit_variants(unit, monkeypatch):
+    """Every unit width of the refactorization kernel (scenarios per warp: 8, 16 or 32)."""
     monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
-    monkeypatch.setenv("B200LU_BATCH_SLOT_KB", str(slot_kb))
-    monkeypatch.setenv("B200LU_BATCH_RING_KB", str(ring_kb))
     fx = kkt_fixture(700, 300, num_systems=4)
     f = BatchedFactors(fx.sym, 33)
     info = f.info
     f.close()
     assert info["unit_scenarios"] == unit
-    if slot_kb == 1:
-        assert info["staged_rows"] < info["factor_rows"]
     _check_batch(fx, 33, refine=False)
+
+
+@needs_ref
+def test_batch_long_pivot_rows_cross_chunks():
+    """A banded matrix with 40 upper entries per row: every pivot row spans three ring chunks."""
+    n, band = 400, 40
+    M = np.zeros((n, n))
+    rng = np.random.default_rng(7)
+    for i in range(n):
+        lo, hi = max(0, i - band), min(n, i + band + 1)
+        M[i, lo:hi] = rng.uniform(-1, 1, hi - lo)
+        M[i, i] = 2.0 * band + 1.0
+    fx = dense_fixture(M)
+    _check_batch(fx, 19, refine=False)
 
 
 @needs_ref
