@@ -49,7 +49,7 @@ struct b200lu_batch {
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
   int32_t batch = 0, padded = 0, groups = 0;
-  int unit = 32;         // scenarios per refactorization unit (S)
+  int unit = 16;         // scenarios per refactorization unit (S)
   int32_t units = 0;     // padded / unit
   int32_t slot_entries = 0, ring_entries = 0;
   bool has_match = false, dest16 = true;
@@ -680,8 +680,8 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   // refactorization unit and shared-memory slot
   {
     const char* e = std::getenv("B200LU_BATCH_UNIT");
-    const int u = e ? std::atoi(e) : 32;
-    h->unit = (u == 8 || u == 16 || u == 32) ? u : 32;
+    const int u = e ? std::atoi(e) : 16;
+    h->unit = (u == 8 || u == 16 || u == 32) ? u : 16;
     h->units = h->padded / h->unit;
   }
 

@@ -172,9 +172,12 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
 // reference's two-rounding update — but the warp never waits for a_ij: no read-modify-write
 // chain, only the streaming loads of row d's upper entries (8 of them, 2 KB per warp, in flight
 // at once) and one load of a_id per pivot for alpha = a_id / u_dd (src/numeric.cpp:40), which the
-// memory model orders after this thread's own earlier reductions to that address. Per-address
-// order is what bit-exactness needs (pivots ascending per slot): with S = 32 one lane owns one
-// scenario, so all operations on an address come from one thread in program order.
+// memory model orders after the earlier reductions to that address. Per-address order is what
+// bit-exactness needs (pivots ascending per slot): with S = 32 one lane owns one scenario and all
+// operations on an address come from one thread in program order; with S < 32 the E = 32/S entry
+// lanes of a scenario take turns on a slot from pivot to pivot, and the __syncwarp() between
+// pivots puts their reductions (and the alpha load) in causality order, which the coherence order
+// of the location must respect.
 template <typename DestT, int S, int kUnroll>
 __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, int lane) {
   constexpr int E = 32 / S;
