@@ -230,6 +230,21 @@ uint64_t b200lu_launch_count(const b200lu_handle* h);
 /* Blocks until everything queued on the handle's stream has finished. */
 b200lu_status b200lu_synchronize(b200lu_handle* h);
 
+/* Device-resident KKT values. assemble_kkt (src/kkt.cpp:53-77) builds
+ * K = [[H + D_y + delta_p I, J^T], [J, -delta_d I]]; across a barrier sequence, and under the
+ * regularization escalation of cli::solve_sequence (src/cli.cpp:148-154: doubled deltas, same
+ * pattern), only K's diagonal changes. After one reset_values / refactorize with the full values,
+ * b200lu_kkt_update rewrites the diagonal on the device exactly as the reference sums it —
+ * K_ii = H_ii + (D_y[i] + delta_p) for the n_primal primal rows, -delta_d for the dual rows — and
+ * scatters, i.e. it replaces reset_values for the next system: 8*n_primal bytes cross the bus
+ * instead of 8*nnz(K), none if D_y already lives on the device. Follow with
+ * b200lu_factorize_scattered. h_diag: H's own diagonal values (0 where H has none), n_primal
+ * doubles; diag_source_pos: position of K_ii in source-CSR order, n entries. */
+b200lu_status b200lu_kkt_bind(b200lu_handle* h, int64_t n_primal, const double* h_diag,
+                              const int64_t* diag_source_pos);
+b200lu_status b200lu_kkt_update(b200lu_handle* h, const double* d_y, int on_device, double delta_p,
+                                double delta_d);
+
 /* ------------------------------------------------------------------------------------------
  * Scenario batches (BASELINE config "batch of 256 independent scenario systems"):
  * `batch` independent systems that share ONE symbolic analysis (same pattern, different values
@@ -250,9 +265,9 @@ typedef struct b200lu_batch b200lu_batch;
 typedef struct {
   int64_t batch, padded_batch;
   int64_t unit_scenarios; /* scenarios a refactorization warp handles at once (8, 16 or 32) */
-  int64_t slot_entries;   /* row length a warp stages in shared memory; longer rows update in place */
+  int64_t blocks;         /* row blocks of the trailing part of the refactorization (kBlockRows rows each) */
   int64_t factor_rows;    /* rows with at least one pivot */
-  int64_t staged_rows, staged_pairs; /* of those, rows (and their update pairs) staged in shared memory */
+  int64_t blocked_rows, blocked_pairs; /* of those, rows (and their update pairs) handled in row blocks */
   int64_t factor_grid, tri_grid;
   int64_t n, nnz_factors, nnz_source, update_pairs, lower_levels, upper_levels;
   int64_t device_bytes, alloc_events, launches;
@@ -293,6 +308,12 @@ b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const
                                          double* x_out, int on_device, int use_preconditioner,
                                          const b200lu_refine_config* cfg,
                                          b200lu_refine_outcome* outcomes);
+/* b200lu_kkt_bind / b200lu_kkt_update for every scenario: d_y is [batch][n_primal]; H, J and the
+ * deltas are shared (scenarios of one network differ in their barrier diagonal and right-hand side). */
+b200lu_status b200lu_batch_kkt_bind(b200lu_batch* h, int64_t n_primal, const double* h_diag,
+                                    const int64_t* diag_source_pos);
+b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on_device, double delta_p,
+                                      double delta_d);
 b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out);
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled);
 b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset);

@@ -203,6 +203,58 @@ void* rluref_gen_sequence(std::int64_t n, std::int64_t m, std::uint64_t topology
   });
   return st == kOk ? seq : nullptr;
 }
+// Same, keeping the per-step KktBlocks (H, J, D_y, deltas: include/rlu/kkt.hpp:14-21) so that the
+// diagonal-only value path and the regularization escalation (src/cli.cpp:148-154) can be checked.
+void* rluref_gen_sequence_blocks(std::int64_t n, std::int64_t m, std::uint64_t topology_seed,
+                                 std::uint64_t y_seed, std::int64_t num_systems, double mu0,
+                                 double mu_min, double reduction, double delta_p, double delta_d) {
+  KktSequence* seq = nullptr;
+  const int st = guarded([&] {
+    GenConfig c;
+    c.n = n;
+    c.m = m;
+    c.topology_seed = topology_seed;
+    c.y_seed = y_seed;
+    c.num_systems = num_systems;
+    c.mu0 = mu0;
+    c.mu_min = mu_min;
+    c.reduction = reduction;
+    c.delta_p = delta_p;
+    c.delta_d = delta_d;
+    seq = new KktSequence(gen_sequence(c));
+  });
+  return st == kOk ? seq : nullptr;
+}
+int rluref_seq_has_blocks(void* s) { return static_cast<KktSequence*>(s)->blocks.empty() ? 0 : 1; }
+std::int64_t rluref_seq_n_primal(void* s) { return static_cast<KktSequence*>(s)->blocks.at(0).H.nrows; }
+// H's own diagonal values (0 where H has no diagonal entry) and D_y / deltas of step k.
+void rluref_seq_h_diag(void* s, std::int64_t k, double* out) {
+  const auto& H = static_cast<KktSequence*>(s)->blocks.at(k).H;
+  for (index_t i = 0; i < H.nrows; ++i) {
+    const index_t t = H.find(i, i);
+    out[i] = t < 0 ? 0.0 : H.values[t];
+  }
+}
+void rluref_seq_dy(void* s, std::int64_t k, double* out) {
+  copy_out(static_cast<KktSequence*>(s)->blocks.at(k).D_y, out);
+}
+void rluref_seq_deltas(void* s, std::int64_t k, double* delta_p, double* delta_d) {
+  const auto& b = static_cast<KktSequence*>(s)->blocks.at(k);
+  *delta_p = b.delta_p;
+  *delta_d = b.delta_d;
+}
+// The regularization step of the escalation policy (src/cli.cpp:53, 148-154): doubles both deltas
+// of step k and re-assembles K in place (same pattern, stronger diagonal).
+int rluref_seq_double_regularization(void* s, std::int64_t k) {
+  return guarded([&] {
+    auto& seq = *static_cast<KktSequence*>(s);
+    KktBlocks& b = seq.blocks.at(k);
+    b.delta_p = b.delta_p == 0.0 ? 1e-12 : 2.0 * b.delta_p;
+    b.delta_d = b.delta_d == 0.0 ? 1e-12 : 2.0 * b.delta_d;
+    KktSystem regged = assemble_kkt(b);
+    seq.systems[k].K = std::move(regged.K);
+  });
+}
 void rluref_seq_destroy(void* s) { delete static_cast<KktSequence*>(s); }
 std::int64_t rluref_seq_num_systems(void* s) {
   return static_cast<std::int64_t>(static_cast<KktSequence*>(s)->systems.size());

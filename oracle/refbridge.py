@@ -71,6 +71,13 @@ def lib():
     sig("rluref_csr_get", None, vp, vp, vp, vp)
     sig("rluref_csr_set_values", None, vp, vp)
     sig("rluref_gen_sequence", vp, i64, i64, u64, u64, i64, dbl, dbl, dbl, dbl, dbl)
+    sig("rluref_gen_sequence_blocks", vp, i64, i64, u64, u64, i64, dbl, dbl, dbl, dbl, dbl)
+    sig("rluref_seq_has_blocks", C.c_int, vp)
+    sig("rluref_seq_n_primal", i64, vp)
+    sig("rluref_seq_h_diag", None, vp, i64, vp)
+    sig("rluref_seq_dy", None, vp, i64, vp)
+    sig("rluref_seq_deltas", None, vp, i64, C.POINTER(dbl), C.POINTER(dbl))
+    sig("rluref_seq_double_regularization", C.c_int, vp, i64)
     sig("rluref_seq_destroy", None, vp)
     sig("rluref_seq_num_systems", i64, vp)
     sig("rluref_seq_n", i64, vp)
@@ -242,9 +249,9 @@ class RefSequence:
     """gen_sequence(GenConfig) — proj/src/kkt.cpp:94-207, defaults proj/include/rlu/kkt.hpp:49-60."""
 
     def __init__(self, n, m, topology_seed=1, y_seed=2, num_systems=0, mu0=1e-1, mu_min=1e-7,
-                 reduction=0.2, delta_p=1e-8, delta_d=1e-8):
-        self._h = lib().rluref_gen_sequence(n, m, topology_seed, y_seed, num_systems, mu0, mu_min,
-                                            reduction, delta_p, delta_d)
+                 reduction=0.2, delta_p=1e-8, delta_d=1e-8, keep_blocks=False):
+        gen = lib().rluref_gen_sequence_blocks if keep_blocks else lib().rluref_gen_sequence
+        self._h = gen(n, m, topology_seed, y_seed, num_systems, mu0, mu_min, reduction, delta_p, delta_d)
         if not self._h:
             raise RefError(ERROR, lib().rluref_last_error().decode())
         self.n_primal, self.m_dual = n, m
@@ -283,6 +290,26 @@ class RefSequence:
 
     def mu(self, k) -> float:
         return float(lib().rluref_seq_mu(self._h, k))
+
+    # -- KktBlocks of step k (include/rlu/kkt.hpp:14-21); only with keep_blocks=True
+    def h_diag(self, k=0) -> np.ndarray:
+        out = np.empty(self.n_primal, dtype=np.float64)
+        lib().rluref_seq_h_diag(self._h, k, _p(out))
+        return out
+
+    def d_y(self, k) -> np.ndarray:
+        out = np.empty(self.n_primal, dtype=np.float64)
+        lib().rluref_seq_dy(self._h, k, _p(out))
+        return out
+
+    def deltas(self, k):
+        dp, dd = C.c_double(), C.c_double()
+        lib().rluref_seq_deltas(self._h, k, C.byref(dp), C.byref(dd))
+        return float(dp.value), float(dd.value)
+
+    def double_regularization(self, k):
+        """The regularization step of cli::solve_sequence's escalation (src/cli.cpp:53, 148-154)."""
+        _check(lib().rluref_seq_double_regularization(self._h, k))
 
     def matrix(self, k) -> RefCsr:
         return RefCsr(lib().rluref_seq_matrix(self._h, k), owned=False, keepalive=self)

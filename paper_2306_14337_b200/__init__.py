@@ -7,13 +7,13 @@ DESIGN.md for the kernels.
 from .solver import (CsrMatrix, DeviceError, DimensionError, Error, FactorOptions, NumericFactors,
                      PatternMismatchError, RefineConfig, RefineOutcome, SymbolicFactors,
                      ZeroPivotError, classic_refine, factorize, factorize_scattered, fgmres_refine,
-                     lower_solve, refactorize, relative_residual, reset_values, scatter_values,
+                     kkt_bind, kkt_update, lower_solve, refactorize, relative_residual, reset_values, scatter_values,
                      solve_system, spmv, upper_solve)
 
 __all__ = [
     "CsrMatrix", "DeviceError", "DimensionError", "Error", "FactorOptions", "NumericFactors",
     "PatternMismatchError", "RefineConfig", "RefineOutcome", "SymbolicFactors", "ZeroPivotError",
-    "classic_refine", "factorize", "factorize_scattered", "fgmres_refine", "lower_solve",
+    "classic_refine", "factorize", "factorize_scattered", "fgmres_refine", "kkt_bind", "kkt_update", "lower_solve",
     "refactorize", "relative_residual", "reset_values", "scatter_values", "solve_system", "spmv",
     "upper_solve",
 ]

@@ -45,8 +45,8 @@ class Stats(C.Structure):
 
 
 class BatchInfo(C.Structure):
-    _fields_ = [(k, i64) for k in ("batch", "padded_batch", "unit_scenarios", "slot_entries", "factor_rows",
-                                   "staged_rows", "staged_pairs", "factor_grid", "tri_grid", "n", "nnz_factors",
+    _fields_ = [(k, i64) for k in ("batch", "padded_batch", "unit_scenarios", "blocks", "factor_rows",
+                                   "blocked_rows", "blocked_pairs", "factor_grid", "tri_grid", "n", "nnz_factors",
                                    "nnz_source", "update_pairs", "lower_levels", "upper_levels", "device_bytes",
                                    "alloc_events", "launches")]
 
@@ -83,6 +83,10 @@ EXPORTS = {
     "b200lu_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
     "b200lu_launch_count": (u64, [vp]),
     "b200lu_synchronize": (i32, [vp]),
+    "b200lu_kkt_bind": (i32, [vp, i64, vp, vp]),
+    "b200lu_kkt_update": (i32, [vp, vp, i32, dbl, dbl]),
+    "b200lu_batch_kkt_bind": (i32, [vp, i64, vp, vp]),
+    "b200lu_batch_kkt_update": (i32, [vp, vp, i32, dbl, dbl]),
     # scenario batches
     "b200lu_batch_create": (i32, [C.POINTER(SymbolicView), C.POINTER(Options), i64, C.POINTER(vp)]),
     "b200lu_batch_destroy": (None, [vp]),

@@ -214,6 +214,21 @@ class BatchedFactors:
         p, dev, keep = self._arr_in(values, len(self.symbolic.scatter_map), "reset_values")
         self._check(_capi.lib().b200lu_batch_reset_values(self._h, p, dev))
 
+    def kkt_bind(self, n_primal: int, h_diag, diag_source_pos):
+        """b200lu_batch_kkt_bind: H's own diagonal and the position of every K_ii in source-CSR order."""
+        hd, pos = rlu._f64(h_diag), rlu._i64(diag_source_pos)
+        if hd.size != n_primal or pos.size != self.symbolic.n:
+            raise rlu.DimensionError("kkt_bind: h_diag needs n_primal entries, diag_source_pos needs n")
+        self._check(_capi.lib().b200lu_batch_kkt_bind(self._h, n_primal, hd.ctypes.data, pos.ctypes.data))
+        self._kkt_n_primal = n_primal
+
+    def kkt_update(self, d_y, delta_p: float, delta_d: float):
+        """assemble_kkt's value path on the device for every scenario (src/kkt.cpp:53-77): d_y is
+        [batch, n_primal]; replaces reset_values for scenarios that differ from the loaded values only
+        in their barrier diagonal / regularization. Follow with factorize_scattered."""
+        p, dev, keep = self._arr_in(d_y, getattr(self, "_kkt_n_primal", -1), "kkt_update")
+        self._check(_capi.lib().b200lu_batch_kkt_update(self._h, p, dev, float(delta_p), float(delta_d)))
+
     def factorize_scattered(self):
         failed = np.full(self.batch, -1, dtype=np.int64)
         self._check(_capi.lib().b200lu_batch_factorize_scattered(self._h, failed.ctypes.data), failed)

@@ -84,6 +84,11 @@ struct b200lu_handle {
   int32_t *d_p = nullptr, *d_pq = nullptr;
   double *d_row_scale = nullptr, *d_col_scale = nullptr;
   int32_t *d_a_row_ptr = nullptr, *d_a_col = nullptr;
+  // device-resident KKT value path (b200lu_kkt_bind)
+  int64_t kkt_n_primal = -1;
+  double *d_kkt_hdiag = nullptr, *d_kkt_dy = nullptr;
+  int32_t* d_kkt_pos = nullptr;
+  bool have_values = false;  // a full set of operator values has been given (reset_values / refactorize)
   // device: values and workspaces
   double *d_a_vals = nullptr, *d_work = nullptr, *d_values = nullptr;
   double *d_w = nullptr, *d_t1 = nullptr, *d_t2 = nullptr;
@@ -981,7 +986,7 @@ void b200lu_destroy(b200lu_handle* h) {
                   h->d_big_meta, h->lower_tail.row, h->lower_tail.entries, h->lower_tail.head_meta,
                   h->lower_tail.head_part_k, h->upper_tail.row, h->upper_tail.entries, h->upper_tail.head_meta,
                   h->upper_tail.head_part_k, h->d_partial, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p,
-                  h->d_pq, h->d_row_scale, h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_a_vals, h->d_work,
+                  h->d_pq, h->d_row_scale, h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_pos, h->d_a_vals, h->d_work,
                   h->d_values, h->d_w, h->d_t1, h->d_t2, h->d_in, h->d_in2, h->d_out, h->d_counters, h->d_failed,
                   h->d_scal, h->d_partials, h->d_ticket, h->d_V, h->d_Z, h->d_wv, h->d_r, h->d_cand, h->d_best,
                   h->d_x0, h->d_b};
@@ -1018,6 +1023,62 @@ b200lu_status b200lu_reset_values(b200lu_handle* h, const double* a_values, int 
                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
   }
   h->valid = false;
+  h->have_values = true;
+  ST_TRY(launch_scatter(h));
+  h->scattered = true;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_kkt_bind(b200lu_handle* h, int64_t n_primal, const double* h_diag,
+                              const int64_t* diag_source_pos) {
+  if (!h || n_primal < 0 || n_primal > h->n || (!h_diag && n_primal) || (!diag_source_pos && h->n)) {
+    return B200LU_INVALID_ARGUMENT;
+  }
+  CU_TRY(h, cudaSetDevice(h->device));
+  std::vector<int32_t> pos(h->n);
+  for (int64_t i = 0; i < h->n; ++i) {
+    const int64_t k = diag_source_pos[i];
+    if (k < h->src_row_offsets[i] || k >= h->src_row_offsets[i + 1] || h->src_col_indices[k] != i) {
+      h->last_error = "kkt_bind: diag_source_pos[" + std::to_string(i) + "] does not address K's diagonal";
+      return B200LU_INVALID_ARGUMENT;
+    }
+    pos[i] = static_cast<int32_t>(k);
+  }
+  for (void* p : {static_cast<void*>(h->d_kkt_hdiag), static_cast<void*>(h->d_kkt_dy), static_cast<void*>(h->d_kkt_pos)}) {
+    if (p) cudaFree(p);
+  }
+  ST_TRY(dev_upload(h, &h->d_kkt_pos, pos));
+  ST_TRY(dev_upload(h, &h->d_kkt_hdiag, std::vector<double>(h_diag, h_diag + n_primal)));
+  ST_TRY(dev_alloc(h, &h->d_kkt_dy, static_cast<size_t>(n_primal)));
+  h->kkt_n_primal = n_primal;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_kkt_update(b200lu_handle* h, const double* d_y, int on_device, double delta_p, double delta_d) {
+  if (!h || (!d_y && h->kkt_n_primal > 0)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->kkt_n_primal < 0 || !h->have_values) {
+    h->last_error = "kkt_update: call b200lu_kkt_bind and give one full set of values (reset_values) first";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  if (delta_p < 0.0 || delta_d < 0.0) {  // src/kkt.cpp:44-46
+    h->last_error = "kkt_update: regularization must be nonnegative";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  const double* dy = d_y;
+  if (!on_device && h->kkt_n_primal > 0) {
+    CU_TRY(h, cudaMemcpyAsync(h->d_kkt_dy, d_y, static_cast<size_t>(h->kkt_n_primal) * sizeof(double),
+                              cudaMemcpyHostToDevice, h->stream));
+    dy = h->d_kkt_dy;
+  }
+  h->valid = false;
+  if (h->n > 0) {
+    PhaseScope ps(h, B200LU_PHASE_SCATTER);
+    kkt_diagonal_kernel<<<blocks_for(h->n, 256), 256, 0, h->stream>>>(static_cast<int32_t>(h->n),
+                                                                      static_cast<int32_t>(h->kkt_n_primal), h->d_kkt_hdiag,
+                                                                      h->d_kkt_pos, dy, delta_p, delta_d, h->d_a_vals);
+    ST_TRY(check_launch(h, "kkt_diagonal_kernel"));
+  }
   ST_TRY(launch_scatter(h));
   h->scattered = true;
   return B200LU_OK;

@@ -60,7 +60,13 @@ struct b200lu_batch {
   int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_diag = nullptr, *d_trivial_rows = nullptr;
   int64_t* d_pair_row_ptr = nullptr;
   FactorMeta* d_factor_meta = nullptr;
-  int32_t n_factor_rows = 0;
+  int32_t n_factor_rows = 0;   // rows with pivots handled row by row (the wide head of the DAG)
+  BlockMeta* d_blocks = nullptr;  // row-blocked trailing part
+  MergedPivot* d_merged = nullptr;
+  int32_t n_blocks = 0, n_block_rows = 0;
+  int64_t blocked_pairs = 0;
+  void (*block_fn)(BBlockArgs) = nullptr;
+  int block_grid = 0;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
@@ -69,6 +75,10 @@ struct b200lu_batch {
   double *d_row_scale = nullptr, *d_col_scale = nullptr;
   int32_t *d_a_row_ptr = nullptr, *d_a_col = nullptr;
 
+  int64_t kkt_n_primal = -1;
+  double *d_kkt_hdiag = nullptr, *d_kkt_dy = nullptr, *d_kkt_stage = nullptr;
+  int32_t* d_kkt_pos = nullptr;
+  bool have_values = false;
   double *d_a_int = nullptr, *d_values = nullptr;
   int32_t* d_flags = nullptr;
   int32_t* d_failed = nullptr;  // [2][padded]: factor (atomicMin), upper (atomicMax)
@@ -262,7 +272,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
         cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
     ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
   }
-  if (h->n_factor_rows > 0) {
+  if (h->n_factor_rows > 0 || h->n_blocks > 0) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
@@ -281,9 +291,29 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
     a.pivot_floor = h->pivot_floor;
     a.failed = h->d_failed;
     a.ticket = h->d_tickets;
-    PhaseScope ps(h, B200LU_PHASE_FACTOR);
+    PhaseScope ps(h, B200LU_PHASE_FACTOR);  // one scope: head launch + blocked trailing launch = one refactorization
     h->factor_fn<<<h->factor_grid, kBWarps * 32, h->factor_smem, h->stream>>>(a);
     ST_TRY(check_launch(h, "bfactor_kernel"));
+    if (h->n_blocks > 0) {
+      BBlockArgs bb;
+      bb.n_blocks = h->n_blocks;
+      bb.units = h->units;
+      bb.gen = h->gen;
+      bb.blocks = h->d_blocks;
+      bb.merged = h->d_merged;
+      bb.row_ptr = h->d_row_ptr;
+      bb.diag = h->d_diag;
+      bb.pair_row_ptr = h->d_pair_row_ptr;
+      bb.dest = h->d_dest;
+      bb.values = h->d_values;
+      bb.nnz_factors = h->nnz_factors;
+      bb.flags = h->d_flags;
+      bb.pivot_floor = h->pivot_floor;
+      bb.failed = h->d_failed;
+      bb.ticket = h->d_tickets + 1;
+      h->block_fn<<<h->block_grid, 256, 0, h->stream>>>(bb);
+      ST_TRY(check_launch(h, "bfactor_block_kernel"));
+    }
   }
   CU_TRY(h, cudaMemcpyAsync(h->h_failed, h->d_failed, static_cast<size_t>(h->padded) * sizeof(int32_t),
                             cudaMemcpyDeviceToHost, h->stream));
@@ -693,13 +723,66 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
   ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
   {
+    // Head / tail split of the refactorization: the maximal suffix of dependency levels narrower
+    // than `tail_width` rows is processed in blocks of kBlockRows consecutive rows (batch.cuh,
+    // bfactor_block_kernel); everything before it row by row. The tail is successor-closed, tail
+    // rows only depend on head rows and on tail rows of smaller index, so [head rows by level]
+    // followed by [tail blocks by index] is a topological order of the claim units.
+    // Measured at C2 x 256: row blocks are SLOWER so far (31-35 ms against 25.6 ms for the factor
+    // phase; blocks of consecutive indices couple independent chains and run at 16 warps per SM),
+    // so the split is off by default; B200LU_BATCH_TAIL_WIDTH (e.g. 64) turns it on.
+    const char* e = std::getenv("B200LU_BATCH_TAIL_WIDTH");
+    const int64_t tail_width = e ? std::atoll(e) : 0;
+    const int64_t levels = static_cast<int64_t>(S.lower_width.size());
+    int64_t cut = levels;
+    for (int64_t l = levels - 1; l >= 1 && S.lower_width[l] < tail_width; --l) cut = l;
+    if (levels - cut < 16) cut = levels;  // not worth a second launch
     std::vector<FactorMeta> meta;
     meta.reserve(n);
+    std::vector<int32_t> tail_rows;
     for (int32_t i : S.lower_order) {  // dependency-level order; rows without pivots are final after the scatter
-      if (S.diag[i] > S.row_ptr[i]) meta.push_back(FactorMeta{i, S.row_ptr[i], S.diag[i], S.row_ptr[i + 1]});
+      if (S.diag[i] == S.row_ptr[i]) continue;
+      if (S.lower_level[i] >= cut) {
+        tail_rows.push_back(i);
+      } else {
+        meta.push_back(FactorMeta{i, S.row_ptr[i], S.diag[i], S.row_ptr[i + 1]});
+      }
     }
     h->n_factor_rows = static_cast<int32_t>(meta.size());
     ST_TRY(dev_upload(h, &h->d_factor_meta, meta));
+    std::sort(tail_rows.begin(), tail_rows.end());
+    std::vector<BlockMeta> blocks;
+    std::vector<MergedPivot> merged;
+    for (size_t b0 = 0; b0 < tail_rows.size(); b0 += kBlockRows) {
+      BlockMeta bm;
+      const int rows_here = static_cast<int>(std::min<size_t>(kBlockRows, tail_rows.size() - b0));
+      std::vector<std::pair<int32_t, int>> piv;  // (pivot row, block row)
+      for (int r = 0; r < kBlockRows; ++r) {
+        bm.row[r] = r < rows_here ? tail_rows[b0 + r] : -1;
+        if (r < rows_here) {
+          const int32_t i = bm.row[r];
+          for (int32_t k = S.row_ptr[i]; k < S.diag[i]; ++k) piv.emplace_back(S.col[k], r);
+        }
+      }
+      std::sort(piv.begin(), piv.end());
+      bm.mbeg = static_cast<int32_t>(merged.size());
+      int last_of_row[kBlockRows];
+      for (int r = 0; r < kBlockRows; ++r) last_of_row[r] = -1;
+      for (size_t q = 0; q < piv.size(); ++q) {
+        if (q == 0 || piv[q].first != piv[q - 1].first) merged.push_back(MergedPivot{piv[q].first, 0u});
+        merged.back().bits |= 1u << piv[q].second;
+        last_of_row[piv[q].second] = static_cast<int>(merged.size()) - 1;
+      }
+      for (int r = 0; r < rows_here; ++r) merged[last_of_row[r]].bits |= 256u << r;
+      bm.mend = static_cast<int32_t>(merged.size());
+      bm.pad0 = bm.pad1 = 0;
+      blocks.push_back(bm);
+    }
+    h->n_blocks = static_cast<int32_t>(blocks.size());
+    h->n_block_rows = static_cast<int32_t>(tail_rows.size());
+    for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+    ST_TRY(dev_upload(h, &h->d_blocks, blocks));
+    ST_TRY(dev_upload(h, &h->d_merged, merged));
   }
   {
     std::vector<int32_t> src_of_slot(nnzF, -1);
@@ -809,6 +892,19 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       return B200LU_CUDA_ERROR;
     }
     h->factor_grid = prop.multiProcessorCount * occ;
+    using BFn = void (*)(BBlockArgs);
+    BFn bfn = nullptr;
+    if (h->dest16) {
+      bfn = h->unit == 8 ? bfactor_block_kernel<uint16_t, 8> : h->unit == 16 ? bfactor_block_kernel<uint16_t, 16>
+                                                                                : bfactor_block_kernel<uint16_t, 32>;
+    } else {
+      bfn = h->unit == 8 ? bfactor_block_kernel<uint32_t, 8> : h->unit == 16 ? bfactor_block_kernel<uint32_t, 16>
+                                                                                : bfactor_block_kernel<uint32_t, 32>;
+    }
+    h->block_fn = bfn;
+    int bocc = 0;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, 0));
+    h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
   }
   {
     int o1 = 0, o2 = 0, o3 = 0;
@@ -840,9 +936,9 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_blocks, h->d_merged, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
-                  h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
+                  h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
                   h->d_x0, h->d_x, h->d_r, h->d_wv, h->d_cand, h->d_best, h->d_V, h->d_Z, h->d_scal, h->d_up, h->d_partials};
   for (void* p : ptrs) {
@@ -873,6 +969,7 @@ b200lu_status b200lu_batch_reset_values(b200lu_batch* h, const double* a_values,
   if (!h || (!a_values && h->nnz_source)) return B200LU_INVALID_ARGUMENT;
   CU_TRY(h, cudaSetDevice(h->device));
   std::fill(h->valid.begin(), h->valid.end(), 0);
+  h->have_values = true;
   const double* src = a_values;
   if (!on_device && h->nnz_source) {
     CU_TRY(h, cudaMemcpyAsync(h->d_stage_a, a_values, static_cast<size_t>(h->nnz_source) * h->batch * sizeof(double),
@@ -886,6 +983,67 @@ b200lu_status b200lu_batch_reset_values(b200lu_batch* h, const double* a_values,
       interleave_kernel<<<grid, 256, 0, h->stream>>>(h->nnz_source, h->batch, src, h->d_a_int);
       ST_TRY(check_launch(h, "interleave_kernel"));
     }
+  }
+  return launch_scatter(h);
+}
+
+b200lu_status b200lu_batch_kkt_bind(b200lu_batch* h, int64_t n_primal, const double* h_diag,
+                                    const int64_t* diag_source_pos) {
+  if (!h || n_primal < 0 || n_primal > h->n || (!h_diag && n_primal) || (!diag_source_pos && h->n)) {
+    return B200LU_INVALID_ARGUMENT;
+  }
+  CU_TRY(h, cudaSetDevice(h->device));
+  std::vector<int32_t> pos(h->n);
+  for (int64_t i = 0; i < h->n; ++i) {
+    const int64_t k = diag_source_pos[i];
+    if (k < h->src_row_offsets[i] || k >= h->src_row_offsets[i + 1] || h->src_col_indices[k] != i) {
+      h->last_error = "kkt_bind: diag_source_pos[" + std::to_string(i) + "] does not address K's diagonal";
+      return B200LU_INVALID_ARGUMENT;
+    }
+    pos[i] = static_cast<int32_t>(k);
+  }
+  for (void* p : {static_cast<void*>(h->d_kkt_hdiag), static_cast<void*>(h->d_kkt_dy), static_cast<void*>(h->d_kkt_stage),
+                  static_cast<void*>(h->d_kkt_pos)}) {
+    if (p) cudaFree(p);
+  }
+  ST_TRY(dev_upload(h, &h->d_kkt_pos, pos));
+  ST_TRY(dev_upload(h, &h->d_kkt_hdiag, std::vector<double>(h_diag, h_diag + n_primal)));
+  ST_TRY(dev_alloc(h, &h->d_kkt_dy, static_cast<size_t>(n_primal) * h->padded));
+  ST_TRY(dev_alloc(h, &h->d_kkt_stage, static_cast<size_t>(n_primal) * h->batch));
+  h->kkt_n_primal = n_primal;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on_device, double delta_p, double delta_d) {
+  if (!h || (!d_y && h->kkt_n_primal > 0)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->kkt_n_primal < 0 || !h->have_values) {
+    h->last_error = "kkt_update: call b200lu_batch_kkt_bind and give one full set of values (reset_values) first";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  if (delta_p < 0.0 || delta_d < 0.0) {  // src/kkt.cpp:44-46
+    h->last_error = "kkt_update: regularization must be nonnegative";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  std::fill(h->valid.begin(), h->valid.end(), 0);
+  const double* src = d_y;
+  if (!on_device && h->kkt_n_primal > 0) {
+    CU_TRY(h, cudaMemcpyAsync(h->d_kkt_stage, d_y, static_cast<size_t>(h->kkt_n_primal) * h->batch * sizeof(double),
+                              cudaMemcpyHostToDevice, h->stream));
+    src = h->d_kkt_stage;
+  }
+  if (h->n > 0) {
+    PhaseScope ps(h, B200LU_PHASE_SCATTER);
+    if (h->kkt_n_primal > 0) {
+      dim3 grid(static_cast<unsigned>((h->kkt_n_primal + 31) / 32), static_cast<unsigned>(h->groups));
+      interleave_kernel<<<grid, 256, 0, h->stream>>>(h->kkt_n_primal, h->batch, src, h->d_kkt_dy);
+      ST_TRY(check_launch(h, "interleave_kernel"));
+    }
+    bkkt_diagonal_kernel<<<warp_blocks(h), 256, 0, h->stream>>>(static_cast<int32_t>(h->n),
+                                                                static_cast<int32_t>(h->kkt_n_primal), h->groups,
+                                                                h->nnz_source, h->d_kkt_hdiag, h->d_kkt_pos, h->d_kkt_dy,
+                                                                delta_p, delta_d, h->d_a_int);
+    ST_TRY(check_launch(h, "bkkt_diagonal_kernel"));
   }
   return launch_scatter(h);
 }
@@ -997,17 +1155,10 @@ b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* ou
   out->batch = h->batch;
   out->padded_batch = h->padded;
   out->unit_scenarios = h->unit;
-  out->slot_entries = h->slot_entries;
-  out->staged_rows = 0;
-  out->staged_pairs = 0;
-  for (int64_t i = 0; i < h->n; ++i) {
-    const int64_t len = h->sched.row_ptr[i + 1] - h->sched.row_ptr[i];
-    if (h->sched.diag[i] > h->sched.row_ptr[i] && len <= h->slot_entries) {
-      ++out->staged_rows;
-      out->staged_pairs += h->sched.pair_row_ptr[i + 1] - h->sched.pair_row_ptr[i];
-    }
-  }
-  out->factor_rows = h->n_factor_rows;
+  out->factor_rows = h->n_factor_rows + h->n_block_rows;
+  out->blocked_rows = h->n_block_rows;
+  out->blocks = h->n_blocks;
+  out->blocked_pairs = h->blocked_pairs;
   out->factor_grid = h->factor_grid;
   out->tri_grid = h->tri_grid;
   out->n = h->n;

@@ -110,6 +110,21 @@ bscatter_kernel(int64_t nnz_factors, int64_t nnz_source, int32_t groups,
   }
 }
 
+// assemble_kkt's diagonal (see kkt_diagonal_kernel, factor.cuh) for every scenario: d_y is
+// interleaved [groups][n_primal][32], the operator values are [groups][nnz_source][32].
+__global__ void __launch_bounds__(256)
+bkkt_diagonal_kernel(int32_t n_total, int32_t n_primal, int32_t groups, int64_t nnz_source,
+                     const double* __restrict__ h_diag, const int32_t* __restrict__ diag_source_pos,
+                     const double* __restrict__ d_y, double delta_p, double delta_d, double* __restrict__ a_int) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n_total) * groups) return;
+  const int64_t g = warp / n_total, i = warp - g * n_total;
+  double v = -delta_d;
+  if (i < n_primal) v = __dadd_rn(__ldg(h_diag + i), __dadd_rn(d_y[(g * n_primal + i) * 32 + lane], delta_p));
+  a_int[(g * nnz_source + __ldg(diag_source_pos + i)) * 32 + lane] = v;
+}
+
 // Pivot check of the rows without a strict-lower entry (elimination leaves them unchanged,
 // src/numeric.cpp:36; the check of src/numeric.cpp:48 still applies).
 __global__ void __launch_bounds__(256)
@@ -265,6 +280,186 @@ bfactor_kernel(const BFactorArgs a) {
     const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.units);
     const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
     bfactor_unit<DestT, S, kUnroll>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, u, lane);
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------ K2 batched, row-blocked trailing part
+//
+// The narrow trailing levels of the elimination DAG (the top of the elimination tree) hold a few
+// per cent of the rows but most of the update pairs, and their rows form chains: consecutive rows
+// share almost all of their pivots, and every row is a pivot of the ones that follow. There a
+// warp owns a BLOCK of kBlockRows consecutive rows (x S scenarios) and walks the ascending merge of
+// their pivot lists: the upper entries of pivot row d are loaded ONCE and applied to every row of
+// the block that has the pivot (each with its own alpha and its own destination slice), which
+// divides the re-reads of the trailing pivot rows — the dominant DRAM traffic of the unblocked
+// kernel — by the block height, and turns most chain hand-offs into program order inside one warp.
+// Per row the pivots are still applied in ascending order with the same two roundings, so the
+// values stay bit-identical. A block row is published as soon as its last pivot has been applied
+// (the host marks that merge position); a pivot that is a row of the same block then finds its
+// flag already set.
+constexpr int kBlockRows = 4;
+
+struct BlockMeta {        // one 32-byte record per block
+  int32_t row[kBlockRows];  // row ids, ascending; -1 pads a short last block
+  int32_t mbeg, mend;       // its merged pivots
+  int32_t pad0, pad1;
+};
+struct MergedPivot {
+  int32_t d;      // pivot row
+  uint32_t bits;  // bit r: block row r has the pivot; bit 8 + r: block row r is final after this pivot
+};
+
+struct BBlockArgs {
+  int32_t n_blocks;
+  int32_t units;
+  int32_t gen;
+  const BlockMeta* blocks;
+  const MergedPivot* merged;
+  const int32_t* row_ptr;
+  const int32_t* diag;
+  const int64_t* pair_row_ptr;
+  const void* dest;
+  double* values;
+  int64_t nnz_factors;
+  int32_t* flags;
+  double pivot_floor;
+  int32_t* failed;
+  unsigned long long* ticket;
+};
+
+template <typename DestT, int S>
+__global__ void __launch_bounds__(256, 2)
+bfactor_block_kernel(const BBlockArgs a) {
+  constexpr int E = 32 / S;
+  constexpr int R = kBlockRows;
+  constexpr int kUnroll = 8;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int s = lane % S, e = lane / S;
+  const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
+  const unsigned long long total = static_cast<unsigned long long>(a.n_blocks) * a.units;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1ull);
+    t = __shfl_sync(full, t, 0);
+    if (t >= total) break;
+    const int32_t b = static_cast<int32_t>(t / a.units);
+    const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units);
+    const int4 b0 = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
+    const int4 b1 = __ldg(reinterpret_cast<const int4*>(a.blocks + b) + 1);
+    const int32_t rows[R] = {b0.x, b0.y, b0.z, b0.w};
+    const int32_t mbeg = b1.x, mend = b1.y;
+    const int32_t sc0 = u * S;
+    double* gbase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31) + s;
+    double* rowg[R];
+    int64_t p[R];
+    int32_t k[R], nl[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int32_t i = max(rows[r], 0);
+      const int32_t lo = __ldg(a.row_ptr + i);
+      rowg[r] = gbase + static_cast<int64_t>(lo) * 32;
+      nl[r] = __ldg(a.diag + i) - lo;
+      p[r] = a.pair_row_ptr[i];
+      k[r] = 0;
+    }
+
+    for (int32_t t0 = mbeg; t0 < mend; t0 += 32) {
+      int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0;
+      uint32_t my_bits = 0;
+      if (t0 + lane < mend) {
+        const int2 mp = __ldg(reinterpret_cast<const int2*>(a.merged) + t0 + lane);
+        my_d = mp.x;
+        my_bits = static_cast<uint32_t>(mp.y);
+        my_dd = __ldg(a.diag + my_d);
+        my_m = __ldg(a.row_ptr + my_d + 1) - my_dd - 1;
+        my_ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my_d) * a.units + u) >= a.gen;
+      }
+      __syncwarp();
+      const int32_t cnt = min(32, mend - t0);
+      for (int32_t q = 0; q < cnt; ++q) {
+        const int32_t dd = __shfl_sync(full, my_dd, q);
+        const int32_t m = __shfl_sync(full, my_m, q);
+        const uint32_t bits = __shfl_sync(full, my_bits, q);
+        if (!__shfl_sync(full, my_ready, q)) {
+          const int32_t d = __shfl_sync(full, my_d, q);
+          const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
+          while (ld_acquire_s32(f) < a.gen) {}
+        }
+        const double* ug = gbase + static_cast<int64_t>(dd) * 32;
+        __syncwarp();  // the entry lanes' reductions of the previous pivot are issued (E > 1)
+        const double udd = ld_cg(ug);
+        double nalpha[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          nalpha[r] = 0.0;
+          if (bits & (1u << r)) nalpha[r] = ld_cg(rowg[r] + static_cast<int64_t>(k[r]) * 32);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) nalpha[r] = -(nalpha[r] / udd);  // src/numeric.cpp:40; the sign is exact
+        int32_t c = e;
+        for (; c + (kUnroll - 1) * E < m; c += kUnroll * E) {
+          // every load of the batch is issued before the first reduction (the reductions are
+          // ordered asm statements: loads placed behind them would wait for nothing but still queue)
+          double uv[kUnroll];
+          int32_t ds[R][kUnroll];
+#pragma unroll
+          for (int j = 0; j < kUnroll; ++j) uv[j] = ld_cg(ug + static_cast<int64_t>(1 + c + j * E) * 32);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int j = 0; j < kUnroll; ++j) ds[r][j] = (bits & (1u << r)) ? dest[p[r] + c + j * E] : 0;
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (bits & (1u << r)) {  // warp-uniform
+#pragma unroll
+              for (int j = 0; j < kUnroll; ++j) {
+                red_add_f64(rowg[r] + static_cast<int64_t>(ds[r][j]) * 32, __dmul_rn(nalpha[r], uv[j]));  // src/numeric.cpp:44
+              }
+            }
+          }
+        }
+        for (; c < m; c += E) {
+          const double uv = ld_cg(ug + static_cast<int64_t>(1 + c) * 32);
+          int32_t ds[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) ds[r] = (bits & (1u << r)) ? dest[p[r] + c] : 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (bits & (1u << r)) red_add_f64(rowg[r] + static_cast<int64_t>(ds[r]) * 32, __dmul_rn(nalpha[r], uv));
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (bits & (1u << r)) {
+            if (e == 0) st_cg(rowg[r] + static_cast<int64_t>(k[r]) * 32, -nalpha[r]);  // l_id, src/numeric.cpp:41
+            p[r] += m;
+            ++k[r];
+          }
+        }
+        if (bits >> 8) {  // rows whose last pivot this was: pivot check (src/numeric.cpp:48) and publication
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (bits & (256u << r)) {
+              if (e == 0 && fabs(ld_cg(rowg[r] + static_cast<int64_t>(nl[r]) * 32)) <= a.pivot_floor) {
+                atomicMin(a.failed + sc0 + s, rows[r]);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (bits & (256u << r)) st_relaxed_s32(a.flags + static_cast<int64_t>(rows[r]) * a.units + u, a.gen);
+            }
+          }
+        }
+      }
+    }
     __syncwarp();
   }
 }

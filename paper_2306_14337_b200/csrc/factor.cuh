@@ -41,6 +41,20 @@ scatter_kernel(int64_t nnz_factors, const int32_t* __restrict__ src_of_slot,
   }
 }
 
+// On-device value path of assemble_kkt (src/kkt.cpp:53-77). Across a barrier sequence, and under
+// the regularization escalation of cli::solve_sequence (src/cli.cpp:148-154), only the diagonal of
+// K = [[H + D_y + delta_p I, J^T], [J, -delta_d I]] changes: the reference sums the two COO
+// entries of a primal diagonal slot, K_ii = H_ii + (D_y[i] + delta_p), and stores -delta_d in the
+// dual ones. The off-diagonal values stay where the last reset_values put them.
+__global__ void __launch_bounds__(256)
+kkt_diagonal_kernel(int32_t n_total, int32_t n_primal, const double* __restrict__ h_diag,
+                    const int32_t* __restrict__ diag_source_pos, const double* __restrict__ d_y, double delta_p,
+                    double delta_d, double* __restrict__ a_values) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_total) return;
+  a_values[diag_source_pos[i]] = i < n_primal ? __dadd_rn(h_diag[i], __dadd_rn(d_y[i], delta_p)) : -delta_d;
+}
+
 // Pivot check of the rows K1 published directly (src/numeric.cpp:48 applies to every row).
 __global__ void __launch_bounds__(256)
 trivial_pivot_kernel(int32_t count, const int32_t* __restrict__ rows, const int32_t* __restrict__ diag,

@@ -432,3 +432,23 @@ def classic_refine(f: NumericFactors, b, x0, config: RefineConfig | None = None,
                    preconditioned: bool = True) -> RefineOutcome:
     """classic_refine, src/refine.cpp:150-188."""
     return _refine("b200lu_refine_classic", f, b, x0, config, preconditioned)
+
+
+def kkt_bind(f: NumericFactors, n_primal: int, h_diag, diag_source_pos):
+    """Prepares the device-resident KKT value path (include/b200lu.h, b200lu_kkt_bind): H's own
+    diagonal and the position of every K_ii in source-CSR order."""
+    hd, pos = _f64(h_diag), _i64(diag_source_pos)
+    if hd.size != n_primal or pos.size != f.symbolic.n:
+        raise DimensionError("kkt_bind: h_diag needs n_primal entries, diag_source_pos needs n")
+    f._check(_capi.lib().b200lu_kkt_bind(f._h, n_primal, hd.ctypes.data, pos.ctypes.data))
+    f._kkt_n_primal = n_primal
+
+
+def kkt_update(f: NumericFactors, d_y, delta_p: float, delta_d: float):
+    """assemble_kkt's value path on the device (src/kkt.cpp:53-77): rewrites K's diagonal from D_y and
+    the regularization shifts and scatters — replaces reset_values for a system that differs from the
+    last one only in its barrier diagonal / regularization. Follow with factorize_scattered."""
+    p, dev, n, keep = f._vec_in(d_y)
+    if n != getattr(f, "_kkt_n_primal", -1):
+        raise DimensionError(f"kkt_update: D_y has length {n}, expected {getattr(f, '_kkt_n_primal', -1)}")
+    f._check(_capi.lib().b200lu_kkt_update(f._h, p, dev, float(delta_p), float(delta_d)))

@@ -93,8 +93,22 @@ def test_batch_unit_variants(unit, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("unit", [16, 32])
+def test_batch_row_blocked_trailing_part(unit, monkeypatch):
+    """The optional row-blocked kernel for the narrow trailing levels (kBlockRows rows per warp)."""
+    monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "64")
+    fx = kkt_fixture(700, 300, num_systems=4)
+    f = BatchedFactors(fx.sym, 17)
+    info = f.info
+    f.close()
+    assert info["blocks"] > 0 and info["blocked_rows"] > 0
+    _check_batch(fx, 17, refine=False)
+
+
+@needs_ref
 def test_batch_long_pivot_rows_cross_chunks():
-    """A banded matrix with 40 upper entries per row: every pivot row spans three ring chunks."""
+    """A banded matrix with 40 upper entries per row: every pivot row spans several load batches."""
     n, band = 400, 40
     M = np.zeros((n, n))
     rng = np.random.default_rng(7)

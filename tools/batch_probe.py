@@ -59,8 +59,8 @@ def main(name, batch, reps=3, check=2, refine_cap=4):
             okv = okv and bool(np.array_equal(f.values(s), ref))
             okx = okx and bool(np.array_equal(xs[s], orc.solve_system(ref, rhs[s])[0]))
     tot = runs[-1]["refactor_ms"] + runs[-1]["solve_ms"] + runs[-1]["refine_ms"]
-    print(json.dumps(dict(name=name, batch=batch, unit=info["unit_scenarios"], slot=info["slot_entries"],
-                          staged_pairs_frac=round(info["staged_pairs"] / max(info["update_pairs"], 1), 3),
+    print(json.dumps(dict(name=name, batch=batch, unit=info["unit_scenarios"], blocks=info["blocks"], blocked_rows=info["blocked_rows"],
+                          blocked_pairs_frac=round(info["blocked_pairs"] / max(info["update_pairs"], 1), 3),
                           grid=info["factor_grid"], fixture_s=round(t_fix, 1), create_s=round(t_create, 2),
                           device_gb=round(info["device_bytes"] / 1e9, 2), runs=runs, lu_bitwise=okv, x_bitwise=okx,
                           worst_relres_final=worst, ms_per_system=round(tot / batch, 4),
