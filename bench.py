@@ -433,11 +433,13 @@ def run_batch(args):
     total_scen = S * world
     mine = scenario_assignment(total_scen, world, rank)
     # ---- input fixture (untimed): one generated scenario per y_seed, one symbolic analysis
-    seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1) for sc in mine]
+    seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1, keep_blocks=True) for sc in mine]
     ref_sym = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
     sym = rlu.SymbolicFactors.from_arrays(ref_sym.arrays())
     ro, ci = seqs[0].pattern()
     N, nnz_a, nnz_f = seqs[0].n, seqs[0].nnz, ref_sym.nnz_factors
+    diag_pos = np.nonzero(np.repeat(np.arange(N), np.diff(ro)) == ci)[0]
+    delta_p, delta_d = seqs[0].deltas(0)
 
     stream = torch.cuda.current_stream()
     f = BatchedFactors(sym, S, rlu.FactorOptions(device=local_rank, stream=stream.cuda_stream,
@@ -446,6 +448,8 @@ def run_batch(args):
     cfg = rlu.RefineConfig(args.refine_maxit, args.refine_tol)
     host_vals = torch.from_numpy(np.stack([q.values(0) for q in seqs])).pin_memory()
     host_rhs = torch.from_numpy(np.stack([q.rhs(0) for q in seqs])).pin_memory()
+    host_dy = torch.from_numpy(np.stack([q.d_y(0) for q in seqs])).pin_memory()  # the scenarios' barrier diagonals
+    f.kkt_bind(n, seqs[0].h_diag(0), diag_pos)
     dev_vals, dev_rhs = host_vals.cuda(), host_rhs.cuda()
     dev_b = torch.empty_like(dev_rhs)
     host_x = torch.empty((S, N), dtype=torch.float64).pin_memory()
@@ -463,6 +467,21 @@ def run_batch(args):
     def step_e2e():
         f.refactorize(host_vals.numpy())          # H2D of the values inside the call
         dev_b.copy_(host_rhs, non_blocking=True)  # rhs H2D on the handle's stream
+        x = f.solve_system(dev_b)
+        its = [0] * S
+        if not args.no_refine:
+            x, outs = f.fgmres_refine(dev_b, x, cfg)
+            its = [o.iterations for o in outs]
+        host_x.copy_(x, non_blocking=True)
+        stream.synchronize()
+        return host_x, its
+
+    def step_e2e_kkt():
+        # the scenarios share H and J and differ in D_y: only D_y and the rhs cross the bus,
+        # the diagonal of every K is rewritten on the device (b200lu_batch_kkt_update)
+        f.kkt_update(host_dy.numpy(), delta_p, delta_d)
+        f.factorize_scattered()
+        dev_b.copy_(host_rhs, non_blocking=True)
         x = f.solve_system(dev_b)
         its = [0] * S
         if not args.no_refine:
@@ -500,6 +519,9 @@ def run_batch(args):
 
     total_ms, iters, phases, launches, clocks = timed(step_resident, args.steps, args.warmup, True)
     e2e_total_ms, _, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2), False)
+    kkt_total_ms, _, _, _, _ = timed(step_e2e_kkt, args.steps, max(1, args.warmup // 2), False)
+    x_kkt, _ = step_e2e_kkt()
+    kkt_same = bool(torch.equal(x_kkt, step_e2e()[0]))  # diagonal-only submission == full-value submission, bit for bit
 
     # ---- per-system records (the fields of SystemRecord, include/rlu/report.hpp:14-27) and a parity
     # spot check against the reference (the checker, not the measured path)
@@ -514,10 +536,10 @@ def run_batch(args):
     f.close()
     allrecs = gather_records(recs, total_scen, device="cuda")
 
-    t = torch.tensor([total_ms, e2e_total_ms, ref_relres], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms, e2e_total_ms, ref_relres, kkt_total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max, e2e_ms_max, relres_max = (float(v) for v in t.cpu())
+    total_ms_max, e2e_ms_max, relres_max, kkt_ms_max = (float(v) for v in t.cpu())
 
     single = None
     if not args.no_single:
@@ -560,6 +582,13 @@ def run_batch(args):
                     "h2d_bytes_per_step": 8 * S * (nnz_a + N), "d2h_bytes_per_step": 8 * S * N,
                     "note": "values + rhs of every scenario from pinned host memory H2D and every x D2H inside the "
                             "timed region, through the public BatchedFactors refactorize/solve_system/fgmres_refine calls"},
+            "e2e_kkt_diagonal": {
+                "value": total_scen * args.steps / (kkt_ms_max / 1000.0), "unit": UNIT,
+                "ms_per_step": kkt_ms_max / args.steps, "h2d_bytes_per_step": 8 * S * (n + N),
+                "d2h_bytes_per_step": 8 * S * N, "bitwise_equal_to_full_value_submission": kkt_same,
+                "note": "same step submitted through the device-resident KKT value path (b200lu_batch_kkt_update, "
+                        "SURVEY 8f-1): the scenarios share H and J, so only each scenario's barrier diagonal D_y "
+                        "(n_primal doubles) and rhs are copied H2D and K's diagonal is rewritten on the device"},
             "gpu_launches": launches,
             "phases_ms_per_step": {p: v[0] / args.steps for p, v in phases.items()},
             "launches_per_step": {p: v[1] / args.steps for p, v in phases.items()},

@@ -57,6 +57,8 @@ def test_no_device_means_no_result():
     h = C.c_void_p()
     st = _capi.lib().b200lu_create(C.byref(_view(fx.sym)), None, C.byref(h))
     assert st == _capi.NO_DEVICE and not h
+    st = _capi.lib().b200lu_batch_create(C.byref(_view(fx.sym)), None, 4, C.byref(h))
+    assert st == _capi.NO_DEVICE and not h
     import paper_2306_14337_b200 as rlu
     with pytest.raises(rlu.DeviceError):
         rlu.NumericFactors(fx.sym)
