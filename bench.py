@@ -364,6 +364,9 @@ def measure_single(args, workload, steps, with_cpu_baseline):
                                tolerance=args.refine_tol)
             tot += o["scatter_ms"] + o["factor_ms"] + o["trisolve_ms"] + o["refine_ms"]
         cpu_ms = tot / reps
+        # the reference's own final residual on the system the parity spot check used (checker only)
+        line["relres_final_reference_same_system"] = float(num.run_system(
+            seq, k_last, refine=not args.no_refine, max_iterations=args.refine_maxit, tolerance=args.refine_tol)["relres_final"])
         line["cpu_baseline"] = {
             "value": 1000.0 / cpu_ms, "unit": UNIT, "ms_per_system": cpu_ms, "cores": policy["threads"],
             "kind": "reference",

@@ -51,7 +51,6 @@ struct b200lu_batch {
   int32_t batch = 0, padded = 0, groups = 0;
   int unit = 16;         // scenarios per refactorization unit (S)
   int32_t units = 0;     // padded / unit
-  int32_t slot_entries = 0, ring_entries = 0;
   bool has_match = false, dest16 = true;
   std::vector<int64_t> src_row_offsets, src_col_indices;
   std::vector<uint8_t> valid;  // per scenario
@@ -276,8 +275,6 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
-    a.slot_entries = h->slot_entries;
-    a.ring_entries = h->ring_entries;
     a.gen = h->gen;
     a.meta = h->d_factor_meta;
     a.row_ptr = h->d_row_ptr;
@@ -881,8 +878,6 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     }
 #undef B200LU_BF
     h->factor_fn = fn;
-    h->slot_entries = 0;
-    h->ring_entries = 0;
     h->factor_smem = 0;
     CU_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->factor_smem)));
     int occ = 0;

@@ -144,22 +144,18 @@ btrivial_pivot_kernel(int32_t count, int32_t groups, int64_t nnz_factors, const 
 //
 // eliminate (src/numeric.cpp:27-58) for S scenarios of one row at a time. A unit of work is
 // (row i, S consecutive scenarios); its warp is laid out as E = 32/S entry lanes x S scenario
-// lanes. Row i of those S scenarios is staged in the warp's shared-memory slot ([entry][S]),
-// the pivots are walked in ascending order exactly as in the reference, and for pivot d the
+// lanes. The pivots are walked in ascending order exactly as in the reference; for pivot d the
 // upper entries of row d are streamed from L2/HBM (E entries x S scenarios = 256 bytes per
-// instruction) and applied through the precomputed destination table. Rows longer than the
-// slot are updated in place in global memory (L1-cached: the row is private to the warp until
-// it is published).
+// instruction) and applied to row i, in place, through the precomputed destination table
+// (bfactor_unit below).
 //
-// Dependencies: one generation counter per (row, unit). The owner writes the finished row,
-// fences, and stores the current generation; consumers acquire it before reading the row's
-// upper entries. Units are claimed in (dependency level, unit) order by persistent warps, so a
-// claimed unit's dependencies are finished or owned by a resident warp.
+// Dependencies: one generation counter per (row, unit). The owner updates the row, fences, and
+// stores the current generation; consumers read the flag before reading the row's upper entries.
+// Units are claimed in (dependency level, unit) order by persistent warps, so a claimed unit's
+// dependencies are finished or owned by a resident warp.
 struct BFactorArgs {
   int32_t n_rows;        // rows that have pivots, in dependency-level order
   int32_t units;         // units per row = padded batch / S
-  int32_t slot_entries;  // row entries a warp's shared-memory slot holds
-  int32_t ring_entries;  // entries (S doubles each) of a warp's pivot-row ring
   int32_t gen;           // generation of this factorization
   const FactorMeta* meta;
   const int32_t* row_ptr;
@@ -294,6 +290,8 @@ bfactor_kernel(const BFactorArgs a) {
 // the block that has the pivot (each with its own alpha and its own destination slice), which
 // divides the re-reads of the trailing pivot rows — the dominant DRAM traffic of the unblocked
 // kernel — by the block height, and turns most chain hand-offs into program order inside one warp.
+// EXPERIMENTAL, off by default (B200LU_BATCH_TAIL_WIDTH): with blocks of consecutive row indices it
+// measures 31-35 ms against 25.6 ms unblocked at C2 x 256 (batch.cu).
 // Per row the pivots are still applied in ascending order with the same two roundings, so the
 // values stay bit-identical. A block row is published as soon as its last pivot has been applied
 // (the host marks that merge position); a pivot that is a row of the same block then finds its
