@@ -867,9 +867,10 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     const char* ev = std::getenv("B200LU_BATCH_VARIANT");
     const int variant = ev ? std::atoi(ev) : 0;
 #define B200LU_BF(T, S) \
-  (variant == 1 ? bfactor_kernel<T, S, kBWarps, 6, 8> : variant == 2 ? bfactor_kernel<T, S, kBWarps, 6, 4> \
-   : variant == 3 ? bfactor_kernel<T, S, kBWarps, 4, 16> : variant == 4 ? bfactor_kernel<T, S, kBWarps, 8, 4> \
-   : variant == 5 ? bfactor_kernel<T, S, kBWarps, 3, 16> : bfactor_kernel<T, S, kBWarps, 4, 8>)
+  (variant == 1 ? bfactor_kernel<T, S, kBWarps, 6, 8, false> : variant == 2 ? bfactor_kernel<T, S, kBWarps, 6, 4, false> \
+   : variant == 3 ? bfactor_kernel<T, S, kBWarps, 4, 16, false> : variant == 4 ? bfactor_kernel<T, S, kBWarps, 3, 8, true> \
+   : variant == 5 ? bfactor_kernel<T, S, kBWarps, 4, 8, true> : variant == 6 ? bfactor_kernel<T, S, kBWarps, 4, 4, true> \
+   : bfactor_kernel<T, S, kBWarps, 4, 8, false>)
     Fn fn = nullptr;
     if (h->dest16) {
       fn = h->unit == 8 ? B200LU_BF(uint16_t, 8) : h->unit == 16 ? B200LU_BF(uint16_t, 16) : B200LU_BF(uint16_t, 32);

@@ -189,7 +189,7 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
 // lanes of a scenario take turns on a slot from pivot to pivot, and the __syncwarp() between
 // pivots puts their reductions (and the alpha load) in causality order, which the coherence order
 // of the location must respect.
-template <typename DestT, int S, int kUnroll>
+template <typename DestT, int S, int kUnroll, bool kPrefetch>
 __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, int lane) {
   constexpr int E = 32 / S;
   const unsigned full = 0xffffffffu;
@@ -214,6 +214,27 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
     }
     __syncwarp();
     const int32_t cnt = min(32, nl - k0);
+    // kPrefetch: the diagonal and the first load batch of the NEXT pivot row (already published
+    // according to the probe) are requested before the current pivot's reductions are issued, so
+    // one memory round trip per pivot leaves the warp's serial path
+    double pf_udd = 0.0, pf_uv[kUnroll];
+    bool pf_ok = false;
+    auto prefetch = [&](int32_t qn) {
+      pf_ok = false;
+      if (kPrefetch && qn < cnt && __shfl_sync(full, my_ready, qn)) {
+        const int32_t ddn = __shfl_sync(full, my_dd, qn);
+        const int32_t mn = __shfl_sync(full, my_m, qn);
+        const double* ugn = gbase + static_cast<int64_t>(ddn) * 32;
+        pf_udd = ld_cg(ugn);
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+          pf_uv[j] = 0.0;
+          if (e + j * E < mn) pf_uv[j] = ld_cg(ugn + static_cast<int64_t>(1 + e + j * E) * 32);
+        }
+        pf_ok = true;
+      }
+    };
+    prefetch(0);
     for (int32_t q = 0; q < cnt; ++q) {
       const int32_t dd = __shfl_sync(full, my_dd, q);
       const int32_t m = __shfl_sync(full, my_m, q);
@@ -225,11 +246,30 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
       const double* ug = gbase + static_cast<int64_t>(dd) * 32;
       const int32_t k = k0 + q;
       if (E > 1) __syncwarp();  // the other entry lanes' reductions of the previous pivot are issued
-      const double udd = ld_cg(ug);
       const double aik = ld_cg(rowg + static_cast<int64_t>(k) * 32);
-      // first batch of row d's upper entries in flight while alpha is being formed
+      double udd, uv0[kUnroll];
+      if (kPrefetch && pf_ok) {
+        udd = pf_udd;
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) uv0[j] = pf_uv[j];
+      } else {
+        udd = ld_cg(ug);
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+          uv0[j] = 0.0;
+          if (e + j * E < m) uv0[j] = ld_cg(ug + static_cast<int64_t>(1 + e + j * E) * 32);
+        }
+      }
+      int32_t ds0[kUnroll];
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) ds0[j] = e + j * E < m ? dest[p + e + j * E] : 0;
+      prefetch(q + 1);
       const double nalpha = -(aik / udd);  // src/numeric.cpp:40; the sign is exact
-      int32_t c = e;
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        if (e + j * E < m) red_add_f64(rowg + static_cast<int64_t>(ds0[j]) * 32, __dmul_rn(nalpha, uv0[j]));  // src/numeric.cpp:44
+      }
+      int32_t c = e + kUnroll * E;
       for (; c + (kUnroll - 1) * E < m; c += kUnroll * E) {
         double uv[kUnroll];
         int32_t ds[kUnroll];
@@ -262,7 +302,7 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
   }
 }
 
-template <typename DestT, int S, int WARPS, int kMinBlocks, int kUnroll>
+template <typename DestT, int S, int WARPS, int kMinBlocks, int kUnroll, bool kPrefetch>
 __global__ void __launch_bounds__(WARPS * 32, kMinBlocks)
 bfactor_kernel(const BFactorArgs a) {
   const int lane = threadIdx.x & 31;
@@ -275,7 +315,7 @@ bfactor_kernel(const BFactorArgs a) {
     const int32_t r = static_cast<int32_t>(t / a.units);
     const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(r) * a.units);
     const int4 m4 = __ldg(reinterpret_cast<const int4*>(a.meta) + r);
-    bfactor_unit<DestT, S, kUnroll>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, u, lane);
+    bfactor_unit<DestT, S, kUnroll, kPrefetch>(a, FactorMeta{m4.x, m4.y, m4.z, m4.w}, u, lane);
     __syncwarp();
   }
 }
