@@ -6,8 +6,8 @@ timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; tail -c 600 gpurun_out/bench_c5.json; tail -5 gpurun_out/bench_c5.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_c5.json 2>> gpurun_out/bench_c5.err; tail -c 300 gpurun_out/bench_ref_c5.json
 python tools/batch_probe.py C3 64 2 > gpurun_out/probe_c3x64.json 2>> gpurun_out/bench_c5.err; tail -c 900 gpurun_out/probe_c3x64.json
-python tools/batch_probe.py C2 64 2 > gpurun_out/probe_c2x64.json 2>> gpurun_out/bench_c5.err; tail -c 500 gpurun_out/probe_c2x64.json
-python tools/batch_probe.py C2 32 2 > gpurun_out/probe_c2x32.json 2>> gpurun_out/bench_c5.err; tail -c 500 gpurun_out/probe_c2x32.json
+
+
 # launch list of the same command (cold-cache, serialised: compare shares)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-single > gpurun_out/ncu_bench.log 2>&1
 tail -3 gpurun_out/ncu_bench.log
