@@ -60,7 +60,11 @@ struct b200lu_batch {
   int64_t* d_pair_row_ptr = nullptr;
   FactorMeta* d_factor_meta = nullptr;
   int32_t n_factor_rows = 0;   // rows with pivots handled row by row (the wide head of the DAG)
-  BlockMeta* d_blocks = nullptr;  // row-blocked trailing part
+  FactorMeta* d_tail_meta = nullptr;  // trailing part row by row (latency-optimised kernel instance)
+  int32_t n_tail_rows = 0;
+  void (*tail_fn)(BFactorArgs) = nullptr;
+  int tail_grid = 0;
+  BlockMeta* d_blocks = nullptr;  // row-blocked trailing part (experimental)
   MergedPivot* d_merged = nullptr;
   int32_t n_blocks = 0, n_block_rows = 0;
   int64_t blocked_pairs = 0;
@@ -271,7 +275,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
         cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
     ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
   }
-  if (h->n_factor_rows > 0 || h->n_blocks > 0) {
+  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
@@ -291,6 +295,13 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
     PhaseScope ps(h, B200LU_PHASE_FACTOR);  // one scope: head launch + blocked trailing launch = one refactorization
     h->factor_fn<<<h->factor_grid, kBWarps * 32, h->factor_smem, h->stream>>>(a);
     ST_TRY(check_launch(h, "bfactor_kernel"));
+    if (h->n_tail_rows > 0) {
+      a.n_rows = h->n_tail_rows;
+      a.meta = h->d_tail_meta;
+      a.ticket = h->d_tickets + 1;
+      h->tail_fn<<<h->tail_grid, kBWarps * 32, 0, h->stream>>>(a);
+      ST_TRY(check_launch(h, "bfactor_kernel<tail>"));
+    }
     if (h->n_blocks > 0) {
       BBlockArgs bb;
       bb.n_blocks = h->n_blocks;
@@ -720,16 +731,22 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
   ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
   {
-    // Head / tail split of the refactorization: the maximal suffix of dependency levels narrower
-    // than `tail_width` rows is processed in blocks of kBlockRows consecutive rows (batch.cuh,
-    // bfactor_block_kernel); everything before it row by row. The tail is successor-closed, tail
-    // rows only depend on head rows and on tail rows of smaller index, so [head rows by level]
-    // followed by [tail blocks by index] is a topological order of the claim units.
-    // Measured at C2 x 256: row blocks are SLOWER so far (31-35 ms against 25.6 ms for the factor
-    // phase; blocks of consecutive indices couple independent chains and run at 16 warps per SM),
-    // so the split is off by default; B200LU_BATCH_TAIL_WIDTH (e.g. 64) turns it on.
+    // Optional head / tail split of the refactorization (EXPERIMENTS, off by default): the maximal
+    // suffix of dependency levels narrower than B200LU_BATCH_TAIL_WIDTH rows (at C2 with 64: levels
+    // 59..983 of 984, 6 383 rows, 77 % of the update pairs — long chains of consecutive rows) runs in
+    // a second launch. The tail is successor-closed, so the head launch has finished every head
+    // pivot before the tail starts.
+    //   B200LU_BATCH_TAIL_MODE=0: the same row-by-row kernel instantiated for latency (24 loads per
+    //           lane in flight, 16 warps per SM). Measured at C2 x 256: 34-37 ms against 25.8 ms
+    //           unsplit — the trailing part needs the throughput of 32 warps per SM as much as short
+    //           hand-offs.
+    //   B200LU_BATCH_TAIL_MODE=1: bfactor_block_kernel, 4 consecutive rows per warp sharing each loaded
+    //           pivot row. Cuts the DRAM traffic of the tail from ~50 GB to 13 GB but its launch takes
+    //           26 ms: 58 % of the stall samples wait on the chain hand-offs.
     const char* e = std::getenv("B200LU_BATCH_TAIL_WIDTH");
     const int64_t tail_width = e ? std::atoll(e) : 0;
+    e = std::getenv("B200LU_BATCH_TAIL_MODE");
+    const int tail_mode = e ? std::atoi(e) : 0;
     const int64_t levels = static_cast<int64_t>(S.lower_width.size());
     int64_t cut = levels;
     for (int64_t l = levels - 1; l >= 1 && S.lower_width[l] < tail_width; --l) cut = l;
@@ -747,6 +764,15 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     }
     h->n_factor_rows = static_cast<int32_t>(meta.size());
     ST_TRY(dev_upload(h, &h->d_factor_meta, meta));
+    if (tail_mode == 0) {  // tail rows in level order through the latency-optimised row kernel
+      std::vector<FactorMeta> tmeta;
+      for (int32_t i : tail_rows) tmeta.push_back(FactorMeta{i, S.row_ptr[i], S.diag[i], S.row_ptr[i + 1]});
+      h->n_tail_rows = static_cast<int32_t>(tmeta.size());
+      ST_TRY(dev_upload(h, &h->d_tail_meta, tmeta));
+      h->n_block_rows = h->n_tail_rows;
+      for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+      tail_rows.clear();
+    }
     std::sort(tail_rows.begin(), tail_rows.end());
     std::vector<BlockMeta> blocks;
     std::vector<MergedPivot> merged;
@@ -776,8 +802,10 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       blocks.push_back(bm);
     }
     h->n_blocks = static_cast<int32_t>(blocks.size());
-    h->n_block_rows = static_cast<int32_t>(tail_rows.size());
-    for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+    if (!tail_rows.empty()) {
+      h->n_block_rows = static_cast<int32_t>(tail_rows.size());
+      for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+    }
     ST_TRY(dev_upload(h, &h->d_blocks, blocks));
     ST_TRY(dev_upload(h, &h->d_merged, merged));
   }
@@ -888,6 +916,20 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       return B200LU_CUDA_ERROR;
     }
     h->factor_grid = prop.multiProcessorCount * occ;
+    {
+      Fn tfn = nullptr;
+      if (h->dest16) {
+        tfn = h->unit == 8 ? bfactor_kernel<uint16_t, 8, kBWarps, 2, 24, false>
+              : h->unit == 16 ? bfactor_kernel<uint16_t, 16, kBWarps, 2, 24, false> : bfactor_kernel<uint16_t, 32, kBWarps, 2, 24, false>;
+      } else {
+        tfn = h->unit == 8 ? bfactor_kernel<uint32_t, 8, kBWarps, 2, 24, false>
+              : h->unit == 16 ? bfactor_kernel<uint32_t, 16, kBWarps, 2, 24, false> : bfactor_kernel<uint32_t, 32, kBWarps, 2, 24, false>;
+      }
+      h->tail_fn = tfn;
+      int tocc = 0;
+      CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tfn, kBWarps * 32, 0));
+      h->tail_grid = prop.multiProcessorCount * std::max(1, tocc);
+    }
     using BFn = void (*)(BBlockArgs);
     BFn bfn = nullptr;
     if (h->dest16) {
@@ -932,7 +974,7 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_blocks, h->d_merged, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
                   h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,

@@ -29,6 +29,16 @@ __device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Spins until the (row, unit) flag reaches `gen`. The poll is paced (sleep doubling from 32 ns to
+// 256 ns): a stalled dependency chain leaves most resident warps waiting, and unpaced polls — tens
+// per microsecond and warp — compete with the working warps for the load/store path.
+__device__ __forceinline__ void wait_flag(const int32_t* f, int32_t gen) {
+  unsigned ns = 32;
+  while (ld_acquire_s32(f) < gen) {
+    __nanosleep(ns);
+    ns = min(ns * 2, 256u);
+  }
+}
 __device__ __forceinline__ void st_relaxed_s32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -241,7 +251,7 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
       if (!__shfl_sync(full, my_ready, q)) {
         const int32_t d = __shfl_sync(full, my_d, q);
         const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
-        while (ld_acquire_s32(f) < a.gen) {}
+        wait_flag(f, a.gen);
       }
       const double* ug = gbase + static_cast<int64_t>(dd) * 32;
       const int32_t k = k0 + q;
@@ -293,13 +303,14 @@ __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorM
 
   // src/numeric.cpp:48: a failing pivot is recorded (lowest row wins) and the row is published
   // anyway so dependents never hang (include/rlu/schedule.hpp:29-33, 82-87)
-  __syncwarp();
-  if (e == 0 && fabs(ld_cg(rowg + static_cast<int64_t>(nl) * 32)) <= a.pivot_floor) atomicMin(a.failed + sc0 + s, i);
+  // The publication comes first (it is what the next row of the chain waits for); the check reads
+  // the final diagonal afterwards.
   __syncwarp();
   if (lane == 0) {
     __threadfence();
     st_relaxed_s32(a.flags + static_cast<int64_t>(i) * a.units + u, a.gen);
   }
+  if (e == 0 && fabs(ld_cg(rowg + static_cast<int64_t>(nl) * 32)) <= a.pivot_floor) atomicMin(a.failed + sc0 + s, i);
 }
 
 template <typename DestT, int S, int WARPS, int kMinBlocks, int kUnroll, bool kPrefetch>
@@ -423,7 +434,7 @@ bfactor_block_kernel(const BBlockArgs a) {
         if (!__shfl_sync(full, my_ready, q)) {
           const int32_t d = __shfl_sync(full, my_d, q);
           const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
-          while (ld_acquire_s32(f) < a.gen) {}
+          wait_flag(f, a.gen);
         }
         const double* ug = gbase + static_cast<int64_t>(dd) * 32;
         __syncwarp();  // the entry lanes' reductions of the previous pivot are issued (E > 1)

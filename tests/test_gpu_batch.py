@@ -93,16 +93,18 @@ def test_batch_unit_variants(unit, monkeypatch):
 
 
 @needs_ref
-@pytest.mark.parametrize("unit", [16, 32])
-def test_batch_row_blocked_trailing_part(unit, monkeypatch):
-    """The optional row-blocked kernel for the narrow trailing levels (kBlockRows rows per warp)."""
+@pytest.mark.parametrize("unit,mode", [(16, 1), (32, 1), (16, 0)])
+def test_batch_split_trailing_part(unit, mode, monkeypatch):
+    """The optional second launch for the narrow trailing levels: mode 1 = row blocks (kBlockRows rows
+    per warp), mode 0 = the row kernel instantiated for latency."""
     monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
     monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "64")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_MODE", str(mode))
     fx = kkt_fixture(700, 300, num_systems=4)
     f = BatchedFactors(fx.sym, 17)
     info = f.info
     f.close()
-    assert info["blocks"] > 0 and info["blocked_rows"] > 0
+    assert info["blocked_rows"] > 0 and (info["blocks"] > 0) == (mode == 1)
     _check_batch(fx, 17, refine=False)
 
 
