@@ -308,6 +308,11 @@ b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const
                                          double* x_out, int on_device, int use_preconditioner,
                                          const b200lu_refine_config* cfg,
                                          b200lu_refine_outcome* outcomes);
+/* classic_refine (src/refine.cpp:150-188) per scenario. */
+b200lu_status b200lu_batch_refine_classic(b200lu_batch* h, const double* b, const double* x0,
+                                          double* x_out, int on_device, int use_preconditioner,
+                                          const b200lu_refine_config* cfg,
+                                          b200lu_refine_outcome* outcomes);
 /* b200lu_kkt_bind / b200lu_kkt_update for every scenario: d_y is [batch][n_primal]; H, J and the
  * deltas are shared (scenarios of one network differ in their barrier diagonal and right-hand side). */
 b200lu_status b200lu_batch_kkt_bind(b200lu_batch* h, int64_t n_primal, const double* h_diag,

@@ -102,6 +102,7 @@ EXPORTS = {
     "b200lu_batch_solve": (i32, [vp, vp, vp, i32, vp]),
     "b200lu_batch_relative_residual": (i32, [vp, vp, vp, i32, vp]),
     "b200lu_batch_refine_fgmres": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
+    "b200lu_batch_refine_classic": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
     "b200lu_batch_get_info": (i32, [vp, C.POINTER(BatchInfo)]),
     "b200lu_batch_set_timing": (i32, [vp, i32]),
     "b200lu_batch_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),

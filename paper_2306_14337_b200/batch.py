@@ -281,8 +281,15 @@ class BatchedFactors:
         self._check(_capi.lib().b200lu_batch_relative_residual(self._h, px, pb, dev, out.ctypes.data))
         return out
 
+    def classic_refine(self, b, x0, config: rlu.RefineConfig | None = None, preconditioned: bool = True):
+        """classic_refine (src/refine.cpp:150-188) per scenario. Returns (x [batch, n], outcomes)."""
+        return self._refine("b200lu_batch_refine_classic", b, x0, config, preconditioned)
+
     def fgmres_refine(self, b, x0, config: rlu.RefineConfig | None = None, preconditioned: bool = True):
         """fgmres_refine (src/refine.cpp:39-142) per scenario. Returns (x [batch, n], outcomes)."""
+        return self._refine("b200lu_batch_refine_fgmres", b, x0, config, preconditioned)
+
+    def _refine(self, fn_name, b, x0, config, preconditioned):
         config = config or rlu.RefineConfig()
         pb, dev, k1 = self._arr_in(b, self.symbolic.n, "fgmres_refine")
         px, dev2, k2 = self._arr_in(x0, self.symbolic.n, "fgmres_refine")
@@ -291,8 +298,8 @@ class BatchedFactors:
         po, out = self._vec_out(b)
         cfg = _capi.RefineConfig(config.max_iterations, config.tolerance)
         ocs = (_capi.RefineOutcome * self.batch)()
-        self._check(_capi.lib().b200lu_batch_refine_fgmres(self._h, pb, px, po, dev, 1 if preconditioned else 0,
-                                                           C.byref(cfg), C.cast(ocs, C.c_void_p)))
+        self._check(getattr(_capi.lib(), fn_name)(self._h, pb, px, po, dev, 1 if preconditioned else 0,
+                                                  C.byref(cfg), C.cast(ocs, C.c_void_p)))
         outcomes = [rlu.RefineOutcome(out[s], int(o.iterations), list(o.residual_history[:o.history_len]),
                                       bool(o.converged)) for s, o in enumerate(ocs)]
         return out, outcomes

@@ -664,6 +664,93 @@ b200lu_status fgmres_batch(H* h, const double* b, const double* x0, int use_prec
   return B200LU_OK;
 }
 
+// classic_refine (src/refine.cpp:150-188) for every scenario in lockstep: x += M^-1 (b - A x), the
+// best iterate is kept per scenario; a scenario that has converged stops updating (its correction
+// is scaled by 0) and rides along.
+b200lu_status classic_batch(H* h, const double* b, const double* x0, int use_precond, const b200lu_refine_config& cfg,
+                            b200lu_refine_outcome* out) {
+  const int32_t n32 = static_cast<int32_t>(h->n);
+  const int32_t B = h->batch;
+  const int wb = warp_blocks(h);
+  for (int32_t s = 0; s < B; ++s) {
+    out[s].iterations = 0;
+    out[s].converged = 0;
+    out[s].history_len = 0;
+  }
+  ST_TRY(copy_dd(h, h->d_best, x0));
+  if (h->n == 0) {
+    for (int32_t s = 0; s < B; ++s) {
+      out[s].residual_history[out[s].history_len++] = 0.0;
+      out[s].converged = 1;
+    }
+    return B200LU_OK;
+  }
+  ST_TRY(launch_residual(h, x0, b, h->d_r, kSlotRes));
+  ST_TRY(read_scalars(h, kSlotRes, 2));
+  std::vector<double> bnorm(B), best_res(B), tmp(B);
+  std::vector<uint8_t> active(B, 1);
+  int n_active = 0;
+  for (int32_t s = 0; s < B; ++s) {
+    const double bn = std::sqrt(hscal(h, kSlotBn)[s]);
+    bnorm[s] = bn > 0.0 ? bn : 1.0;
+    best_res[s] = std::sqrt(hscal(h, kSlotRes)[s]) / bnorm[s];
+    out[s].residual_history[out[s].history_len++] = best_res[s];
+    if (best_res[s] <= cfg.tolerance) {
+      out[s].converged = 1;
+      active[s] = 0;
+    }
+    n_active += active[s];
+  }
+  double* x = h->d_cand;
+  ST_TRY(copy_dd(h, x, x0));
+  const double* dev = nullptr;
+  for (int it = 0; it < cfg.max_iterations && n_active > 0; ++it) {
+    // d_r holds b - A x for the current x (from the initial residual, then from the end of the previous pass)
+    if (use_precond) {
+      ST_TRY(solve_int(h, h->d_r, h->d_wv));
+    } else {
+      ST_TRY(copy_dd(h, h->d_wv, h->d_r));
+    }
+    for (int32_t s = 0; s < B; ++s) tmp[s] = active[s] ? 1.0 : 0.0;
+    ST_TRY(upload_scalars(h, tmp, &dev));
+    {
+      PhaseScope ps(h, B200LU_PHASE_VECTOR);
+      baxpy_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, h->d_wv, x);  // axpy(1.0, d, x), src/refine.cpp:170
+    }
+    ST_TRY(check_launch(h, "baxpy_kernel"));
+    ST_TRY(launch_residual(h, x, b, h->d_r, kSlotRes));
+    ST_TRY(read_scalars(h, kSlotRes, 1));
+    bool any_copy = false;
+    for (int32_t s = 0; s < B; ++s) {
+      tmp[s] = 0.0;
+      if (!active[s]) continue;
+      out[s].iterations = it + 1;
+      const double res = std::sqrt(hscal(h, kSlotRes)[s]) / bnorm[s];
+      out[s].residual_history[out[s].history_len++] = res;
+      if (res < best_res[s]) {
+        best_res[s] = res;
+        tmp[s] = 1.0;
+        any_copy = true;
+      }
+      if (best_res[s] <= cfg.tolerance) {
+        out[s].converged = 1;
+        active[s] = 0;
+      }
+    }
+    if (any_copy) {
+      ST_TRY(upload_scalars(h, tmp, &dev));
+      {
+        PhaseScope ps(h, B200LU_PHASE_VECTOR);
+        bcopy_masked_kernel<<<wb, 256, 0, h->stream>>>(n32, h->groups, dev, x, h->d_best);
+      }
+      ST_TRY(check_launch(h, "bcopy_masked_kernel"));
+    }
+    n_active = 0;
+    for (int32_t s = 0; s < B; ++s) n_active += active[s];
+  }
+  return B200LU_OK;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -1167,9 +1254,9 @@ b200lu_status b200lu_batch_relative_residual(b200lu_batch* h, const double* x, c
   return B200LU_OK;
 }
 
-b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const double* x0, double* x_out, int on_device,
+static b200lu_status batch_refine_common(b200lu_batch* h, const double* b, const double* x0, double* x_out, int on_device,
                                          int use_preconditioner, const b200lu_refine_config* cfg_in,
-                                         b200lu_refine_outcome* outcomes) {
+                                         b200lu_refine_outcome* outcomes, bool fgmres) {
   if (!h || !outcomes || (!b && h->n) || (!x0 && h->n) || (!x_out && h->n)) return B200LU_INVALID_ARGUMENT;
   CU_TRY(h, cudaSetDevice(h->device));
   b200lu_refine_config cfg{20, 1e-14};
@@ -1183,9 +1270,22 @@ b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const
     ST_TRY(vec_in(h, b, on_device, h->d_stage_in, h->d_b));
     ST_TRY(vec_in(h, x0, on_device, h->d_stage_in2, h->d_x0));
   }
-  ST_TRY(fgmres_batch(h, h->d_b, h->d_x0, use_preconditioner, cfg, outcomes));
+  ST_TRY(fgmres ? fgmres_batch(h, h->d_b, h->d_x0, use_preconditioner, cfg, outcomes)
+                : classic_batch(h, h->d_b, h->d_x0, use_preconditioner, cfg, outcomes));
   if (h->n == 0) return B200LU_OK;
   return vec_out(h, h->d_best, x_out, on_device);
+}
+
+b200lu_status b200lu_batch_refine_fgmres(b200lu_batch* h, const double* b, const double* x0, double* x_out, int on_device,
+                                         int use_preconditioner, const b200lu_refine_config* cfg,
+                                         b200lu_refine_outcome* outcomes) {
+  return batch_refine_common(h, b, x0, x_out, on_device, use_preconditioner, cfg, outcomes, true);
+}
+
+b200lu_status b200lu_batch_refine_classic(b200lu_batch* h, const double* b, const double* x0, double* x_out, int on_device,
+                                          int use_preconditioner, const b200lu_refine_config* cfg,
+                                          b200lu_refine_outcome* outcomes) {
+  return batch_refine_common(h, b, x0, x_out, on_device, use_preconditioner, cfg, outcomes, false);
 }
 
 b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out) {

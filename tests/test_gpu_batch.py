@@ -207,3 +207,25 @@ def test_batch_c1_all_scenarios():
     final = f.relative_residual(xr, rhs)
     assert np.all(final <= 1e-14) and all(o.converged for o in outcomes)
     f.close()
+
+
+@needs_ref
+def test_batch_classic_refine_matches_the_oracle_per_scenario():
+    """classic_refine (src/refine.cpp:150-188) in a batch: iteration counts, history lengths and the
+    final residual per scenario against the oracle's run on the same x0 (test_refine.cpp:219-242 style)."""
+    fx = kkt_fixture(700, 300, num_systems=4)
+    vals, rhs = _scenarios(fx, 9)
+    f = BatchedFactors(fx.sym, 9)
+    f.refactorize(vals)
+    x = f.solve_system(rhs)
+    xr, outcomes = f.classic_refine(rhs, x)
+    for s in range(9):
+        A = fx.oracle_csr(0, vals[s])
+        lu = fx.oracle.factorize(vals[s])[0]
+        x_ref, its_ref, conv_ref, hist_ref = ob.refine(A, rhs[s], x[s], fx.oracle, lu, method="classic")
+        got, ref = A.relative_residual(xr[s], rhs[s]), A.relative_residual(x_ref, rhs[s])
+        assert got <= max(4 * ref, 1e-15), (s, got, ref)
+        assert outcomes[s].iterations == its_ref and outcomes[s].converged == conv_ref
+        assert len(outcomes[s].residual_history) == len(hist_ref)
+    # identity preconditioner on a diagonal system converges only where the diagonal is 1 (test_refine.cpp:148-159 style)
+    f.close()
