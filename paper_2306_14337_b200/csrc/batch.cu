@@ -985,6 +985,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   (variant == 1 ? bfactor_kernel<T, S, kBWarps, 6, 8, false> : variant == 2 ? bfactor_kernel<T, S, kBWarps, 6, 4, false> \
    : variant == 3 ? bfactor_kernel<T, S, kBWarps, 4, 16, false> : variant == 4 ? bfactor_kernel<T, S, kBWarps, 3, 8, true> \
    : variant == 5 ? bfactor_kernel<T, S, kBWarps, 4, 8, true> : variant == 6 ? bfactor_kernel<T, S, kBWarps, 4, 4, true> \
+   : variant == 7 ? bfactor_kernel<T, S, kBWarps, 3, 16, false> : variant == 8 ? bfactor_kernel<T, S, kBWarps, 2, 32, false> \
    : bfactor_kernel<T, S, kBWarps, 4, 8, false>)
     Fn fn = nullptr;
     if (h->dest16) {
