@@ -12,7 +12,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <queue>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "batch.cuh"
@@ -49,7 +52,7 @@ struct b200lu_batch {
   Schedule sched;
   int64_t n = 0, nnz_factors = 0, nnz_source = 0;
   int32_t batch = 0, padded = 0, groups = 0;
-  int unit = 16;         // scenarios per refactorization unit (S)
+  int unit = 32;         // scenarios per refactorization unit (S): one lane per scenario
   int32_t units = 0;     // padded / unit
   bool has_match = false, dest16 = true;
   std::vector<int64_t> src_row_offsets, src_col_indices;
@@ -802,13 +805,13 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   h->src_row_offsets.assign(sym->source_row_offsets, sym->source_row_offsets + n + 1);
   h->src_col_indices.assign(sym->source_col_indices, sym->source_col_indices + nnzA);
 
-  // refactorization unit and shared-memory slot
-  {
-    const char* e = std::getenv("B200LU_BATCH_UNIT");
-    const int u = e ? std::atoi(e) : 16;
-    h->unit = (u == 8 || u == 16 || u == 32) ? u : 16;
-    h->units = h->padded / h->unit;
-  }
+  // Refactorization unit: 32 scenarios per warp, lane = scenario (E = 1). Narrower units (two or four
+  // entry lanes per scenario) are faster by ~10 % but NOT safe with reduction updates: the reductions
+  // and loads that different lanes of a warp issue to one address are not kept in order by the
+  // hardware (found with the B200LU_POLL_ATOMIC stress build), so all operations on a
+  // value must come from one thread.
+  h->unit = 32;
+  h->units = h->padded / h->unit;
 
   ST_TRY(dev_upload(h, &h->d_row_ptr, S.row_ptr));
   ST_TRY(dev_upload(h, &h->d_col, S.col));
@@ -887,6 +890,53 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       bm.mend = static_cast<int32_t>(merged.size());
       bm.pad0 = bm.pad1 = 0;
       blocks.push_back(bm);
+    }
+    if (!blocks.empty()) {
+      // Claim order of the blocks. Index order is topological (a trailing row only depends on rows of
+      // smaller index) but walks ONE chain at a time — consecutive indices are one chain — so the
+      // resident warps would all sit on the same sequential chain. Level order interleaves the chains
+      // but is not topological for blocks (a block spans several levels). Hence: Kahn's algorithm on
+      // the block DAG with the ready blocks taken by (level of first row, index).
+      const size_t nb = blocks.size();
+      std::vector<int32_t> block_of(n, -1);
+      for (size_t b = 0; b < nb; ++b) {
+        for (int r = 0; r < kBlockRows; ++r) {
+          if (blocks[b].row[r] >= 0) block_of[blocks[b].row[r]] = static_cast<int32_t>(b);
+        }
+      }
+      std::vector<std::vector<int32_t>> succ(nb);
+      std::vector<int32_t> indeg(nb, 0);
+      for (size_t b = 0; b < nb; ++b) {
+        int32_t last = -1;  // merged pivots ascend, so the blocks they belong to ascend too
+        for (int32_t t = blocks[b].mbeg; t < blocks[b].mend; ++t) {
+          const int32_t pb = block_of[merged[t].d];
+          if (pb >= 0 && pb != static_cast<int32_t>(b) && pb != last) {
+            succ[pb].push_back(static_cast<int32_t>(b));
+            ++indeg[b];
+            last = pb;
+          }
+        }
+      }
+      using Key = std::pair<int32_t, int32_t>;  // (level of first row, block id), smallest first
+      std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
+      for (size_t b = 0; b < nb; ++b) {
+        if (indeg[b] == 0) ready.emplace(S.lower_level[blocks[b].row[0]], static_cast<int32_t>(b));
+      }
+      std::vector<BlockMeta> ordered;
+      ordered.reserve(nb);
+      while (!ready.empty()) {
+        const int32_t b = ready.top().second;
+        ready.pop();
+        ordered.push_back(blocks[b]);
+        for (int32_t c : succ[b]) {
+          if (--indeg[c] == 0) ready.emplace(S.lower_level[blocks[c].row[0]], c);
+        }
+      }
+      if (ordered.size() != nb) {
+        h->last_error = "row-block dependency graph is not acyclic";
+        return B200LU_INVALID_ARGUMENT;
+      }
+      blocks.swap(ordered);
     }
     h->n_blocks = static_cast<int32_t>(blocks.size());
     if (!tail_rows.empty()) {
@@ -987,12 +1037,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
    : variant == 5 ? bfactor_kernel<T, S, kBWarps, 4, 8, true> : variant == 6 ? bfactor_kernel<T, S, kBWarps, 4, 4, true> \
    : variant == 7 ? bfactor_kernel<T, S, kBWarps, 3, 16, false> : variant == 8 ? bfactor_kernel<T, S, kBWarps, 2, 32, false> \
    : bfactor_kernel<T, S, kBWarps, 4, 8, false>)
-    Fn fn = nullptr;
-    if (h->dest16) {
-      fn = h->unit == 8 ? B200LU_BF(uint16_t, 8) : h->unit == 16 ? B200LU_BF(uint16_t, 16) : B200LU_BF(uint16_t, 32);
-    } else {
-      fn = h->unit == 8 ? B200LU_BF(uint32_t, 8) : h->unit == 16 ? B200LU_BF(uint32_t, 16) : B200LU_BF(uint32_t, 32);
-    }
+    Fn fn = h->dest16 ? B200LU_BF(uint16_t, 32) : B200LU_BF(uint32_t, 32);
 #undef B200LU_BF
     h->factor_fn = fn;
     h->factor_smem = 0;
@@ -1005,28 +1050,14 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     }
     h->factor_grid = prop.multiProcessorCount * occ;
     {
-      Fn tfn = nullptr;
-      if (h->dest16) {
-        tfn = h->unit == 8 ? bfactor_kernel<uint16_t, 8, kBWarps, 2, 24, false>
-              : h->unit == 16 ? bfactor_kernel<uint16_t, 16, kBWarps, 2, 24, false> : bfactor_kernel<uint16_t, 32, kBWarps, 2, 24, false>;
-      } else {
-        tfn = h->unit == 8 ? bfactor_kernel<uint32_t, 8, kBWarps, 2, 24, false>
-              : h->unit == 16 ? bfactor_kernel<uint32_t, 16, kBWarps, 2, 24, false> : bfactor_kernel<uint32_t, 32, kBWarps, 2, 24, false>;
-      }
+      Fn tfn = h->dest16 ? bfactor_kernel<uint16_t, 32, kBWarps, 2, 24, false> : bfactor_kernel<uint32_t, 32, kBWarps, 2, 24, false>;
       h->tail_fn = tfn;
       int tocc = 0;
       CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tfn, kBWarps * 32, 0));
       h->tail_grid = prop.multiProcessorCount * std::max(1, tocc);
     }
     using BFn = void (*)(BBlockArgs);
-    BFn bfn = nullptr;
-    if (h->dest16) {
-      bfn = h->unit == 8 ? bfactor_block_kernel<uint16_t, 8> : h->unit == 16 ? bfactor_block_kernel<uint16_t, 16>
-                                                                                : bfactor_block_kernel<uint16_t, 32>;
-    } else {
-      bfn = h->unit == 8 ? bfactor_block_kernel<uint32_t, 8> : h->unit == 16 ? bfactor_block_kernel<uint32_t, 16>
-                                                                                : bfactor_block_kernel<uint32_t, 32>;
-    }
+    BFn bfn = h->dest16 ? bfactor_block_kernel<uint16_t, 32> : bfactor_block_kernel<uint32_t, 32>;
     h->block_fn = bfn;
     int bocc = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, 0));

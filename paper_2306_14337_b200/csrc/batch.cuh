@@ -32,9 +32,16 @@ __device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
 // Spins until the (row, unit) flag reaches `gen`. The poll is paced (sleep doubling from 32 ns to
 // 256 ns): a stalled dependency chain leaves most resident warps waiting, and unpaced polls — tens
 // per microsecond and warp — compete with the working warps for the load/store path.
+__device__ __forceinline__ int32_t ld_flag_poll(const int32_t* p) {
+#ifdef B200LU_POLL_ATOMIC
+  return atomicOr(const_cast<int32_t*>(p), 0);
+#else
+  return ld_acquire_s32(p);
+#endif
+}
 __device__ __forceinline__ void wait_flag(const int32_t* f, int32_t gen) {
   unsigned ns = 32;
-  while (ld_acquire_s32(f) < gen) {
+  while (ld_flag_poll(f) < gen) {
     __nanosleep(ns);
     ns = min(ns * 2, 256u);
   }
@@ -193,12 +200,14 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
 // reference's two-rounding update — but the warp never waits for a_ij: no read-modify-write
 // chain, only the streaming loads of row d's upper entries (8 of them, 2 KB per warp, in flight
 // at once) and one load of a_id per pivot for alpha = a_id / u_dd (src/numeric.cpp:40), which the
-// memory model orders after the earlier reductions to that address. Per-address order is what
-// bit-exactness needs (pivots ascending per slot): with S = 32 one lane owns one scenario and all
-// operations on an address come from one thread in program order; with S < 32 the E = 32/S entry
-// lanes of a scenario take turns on a slot from pivot to pivot, and the __syncwarp() between
-// pivots puts their reductions (and the alpha load) in causality order, which the coherence order
-// of the location must respect.
+// hardware orders after THIS THREAD's earlier reductions to that address. Per-address order is what
+// bit-exactness needs (pivots ascending per slot), and it is only safe when every operation on an
+// address comes from one thread: the kernel is instantiated with S = 32 (one lane per scenario,
+// E = 1). With S < 32 the entry lanes of a scenario take turns on a slot from pivot to pivot with a
+// __syncwarp() in between, which measured ~10 % faster and passed every parity test — but a
+// reduction and a later load (or reduction) issued by DIFFERENT lanes of the warp can overtake each
+// other on the way to L2: the B200LU_POLL_ATOMIC stress build (slow, atomic flag polls) turns that
+// into wrong, run-to-run different values in the last rows at S = 8/16 and never at S = 32.
 template <typename DestT, int S, int kUnroll, bool kPrefetch>
 __device__ __forceinline__ void bfactor_unit(const BFactorArgs& a, const FactorMeta mt, int32_t u, int lane) {
   constexpr int E = 32 / S;

@@ -80,31 +80,17 @@ def test_batch_two_groups_partial():
 
 
 @needs_ref
-@pytest.mark.parametrize("unit", [8, 16, 32])
-def test_batch_unit_variants(unit, monkeypatch):
-    """Every unit width of the refactorization kernel (scenarios per warp: 8, 16 or 32)."""
-    monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
-    fx = kkt_fixture(700, 300, num_systems=4)
-    f = BatchedFactors(fx.sym, 33)
-    info = f.info
-    f.close()
-    assert info["unit_scenarios"] == unit
-    _check_batch(fx, 33, refine=False)
-
-
-@needs_ref
-@pytest.mark.parametrize("unit,mode", [(16, 1), (32, 1), (16, 0)])
-def test_batch_split_trailing_part(unit, mode, monkeypatch):
+@pytest.mark.parametrize("mode", [1, 0])
+def test_batch_split_trailing_part(mode, monkeypatch):
     """The optional second launch for the narrow trailing levels: mode 1 = row blocks (kBlockRows rows
     per warp), mode 0 = the row kernel instantiated for latency."""
-    monkeypatch.setenv("B200LU_BATCH_UNIT", str(unit))
     monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "64")
     monkeypatch.setenv("B200LU_BATCH_TAIL_MODE", str(mode))
     fx = kkt_fixture(700, 300, num_systems=4)
     f = BatchedFactors(fx.sym, 17)
     info = f.info
     f.close()
-    assert info["blocked_rows"] > 0 and (info["blocks"] > 0) == (mode == 1)
+    assert info["unit_scenarios"] == 32 and info["blocked_rows"] > 0 and (info["blocks"] > 0) == (mode == 1)
     _check_batch(fx, 17, refine=False)
 
 

@@ -75,6 +75,12 @@ def test_batch_bitwise_at_c2():
         ref, failed = fx.oracle.factorize(vals[s])
         assert failed == -1 and np.array_equal(f.values(s), ref)
         assert np.array_equal(x[s], fx.oracle.solve_system(ref, rhs[s])[0])
+    # run-to-run determinism of the refactorization (its updates are L2 reductions, ordered per thread):
+    # the rows at the top of the elimination tree — the longest dependency chains — are where a race shows
+    before = {s: f.values(s) for s in (0, 7, 21, 47)}
+    f.refactorize(vals)
+    for s, v in before.items():
+        assert np.array_equal(f.values(s), v)
     xr, outs = f.fgmres_refine(rhs, x, rlu.RefineConfig(max_iterations=4))
     final = f.relative_residual(xr, rhs)
     assert np.all(final <= 1e-14) and all(o.converged and o.iterations <= 2 for o in outs)

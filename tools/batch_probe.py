@@ -1,7 +1,7 @@
 """Dev tool (GPU box): phase breakdown of the interleaved scenario-batch path.
 
     python tools/batch_probe.py C2 256 [reps]
-Environment: B200LU_BATCH_UNIT (8/16/32), B200LU_BATCH_SLOT_KB."""
+Environment: B200LU_BATCH_VARIANT, B200LU_BATCH_TAIL_WIDTH / B200LU_BATCH_TAIL_MODE (experiments)."""
 import os, sys, time, json
 import numpy as np
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
