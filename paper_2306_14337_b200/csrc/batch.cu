@@ -827,7 +827,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     // a second launch. The tail is successor-closed, so the head launch has finished every head
     // pivot before the tail starts.
     //   B200LU_BATCH_TAIL_MODE=0: the same row-by-row kernel instantiated for latency (24 loads per
-    //           lane in flight, 16 warps per SM). Measured at C2 x 256: 34-37 ms against 25.8 ms
+    //           lane in flight, 16 warps per SM). Measured at C2 x 256: 34-37 ms against 28.9 ms
     //           unsplit — the trailing part needs the throughput of 32 warps per SM as much as short
     //           hand-offs.
     //   B200LU_BATCH_TAIL_MODE=1: bfactor_block_kernel, 4 consecutive rows per warp sharing each loaded

@@ -351,7 +351,7 @@ bfactor_kernel(const BFactorArgs a) {
 // divides the re-reads of the trailing pivot rows — the dominant DRAM traffic of the unblocked
 // kernel — by the block height, and turns most chain hand-offs into program order inside one warp.
 // EXPERIMENTAL, off by default (B200LU_BATCH_TAIL_WIDTH): with blocks of consecutive row indices it
-// measures 31-35 ms against 25.6 ms unblocked at C2 x 256 (batch.cu).
+// measures 32-34 ms against 28.9 ms unblocked at C2 x 256 (batch.cu).
 // Per row the pivots are still applied in ascending order with the same two roundings, so the
 // values stay bit-identical. A block row is published as soon as its last pivot has been applied
 // (the host marks that merge position); a pivot that is a row of the same block then finds its
