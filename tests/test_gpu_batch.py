@@ -80,6 +80,24 @@ def test_batch_two_groups_partial():
 
 
 @needs_ref
+@pytest.mark.parametrize("batch", [1, 32])
+def test_batch_sizes_one_and_exactly_one_group(batch):
+    _check_batch(kkt_fixture(700, 300, num_systems=4), batch)
+
+
+@needs_ref
+def test_batch_one_by_one_matrix():
+    fx = dense_fixture(np.array([[2.0]]))
+    f = BatchedFactors(fx.sym, 3)
+    f.refactorize(np.array([[2.0], [4.0], [-8.0]]))
+    x = f.solve_system(np.array([[1.0], [1.0], [1.0]]))
+    assert np.array_equal(x, np.array([[0.5], [0.25], [-0.125]]))
+    xr, outs = f.fgmres_refine(np.ones((3, 1)), x)
+    assert np.array_equal(xr, x) and all(o.converged and o.iterations == 0 for o in outs)
+    f.close()
+
+
+@needs_ref
 @pytest.mark.parametrize("mode", [1, 0])
 def test_batch_split_trailing_part(mode, monkeypatch):
     """The optional second launch for the narrow trailing levels: mode 1 = row blocks (kBlockRows rows
