@@ -696,9 +696,19 @@ def run_b200(args):
     rank, local_rank, world = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device — the b200lu path has no CPU fallback")
+    # One rank per GPU over NCCL. Test hook for boxes with a single GPU (the multi-rank control flow —
+    # scenario assignment, barriers, max-over-ranks, record gather — can then be exercised with
+    # `B200LU_BENCH_ONE_DEVICE=1 torchrun --nproc-per-node 2 ...`): every rank uses cuda:0 and gloo.
+    one_device = os.environ.get("B200LU_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        os.environ["LOCAL_RANK"] = "0"
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.workload == BATCH_WORKLOAD:
         run_batch(args)
         return
