@@ -821,22 +821,24 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   ST_TRY(dev_upload(h, &h->d_lower_meta, S.lower_meta));
   ST_TRY(dev_upload(h, &h->d_upper_meta, S.upper_meta));
   {
-    // Optional head / tail split of the refactorization (EXPERIMENTS, off by default): the maximal
-    // suffix of dependency levels narrower than B200LU_BATCH_TAIL_WIDTH rows (at C2 with 64: levels
-    // 59..983 of 984, 6 383 rows, 77 % of the update pairs — long chains of consecutive rows) runs in
-    // a second launch. The tail is successor-closed, so the head launch has finished every head
-    // pivot before the tail starts.
-    //   B200LU_BATCH_TAIL_MODE=0: the same row-by-row kernel instantiated for latency (24 loads per
-    //           lane in flight, 16 warps per SM). Measured at C2 x 256: 34-37 ms against 28.9 ms
-    //           unsplit — the trailing part needs the throughput of 32 warps per SM as much as short
-    //           hand-offs.
-    //   B200LU_BATCH_TAIL_MODE=1: bfactor_block_kernel, 4 consecutive rows per warp sharing each loaded
-    //           pivot row. Cuts the DRAM traffic of the tail from ~50 GB to 13 GB but its launch takes
-    //           26 ms: 58 % of the stall samples wait on the chain hand-offs.
+    // Head / tail split of the refactorization. The maximal suffix of dependency levels narrower than
+    // `tail_width` rows runs in a second launch; it is successor-closed, so the head launch has
+    // finished every head pivot before it starts. Below the first few dozen levels the elimination DAG
+    // consists of chains of index-consecutive rows in which every row is a pivot of the next and
+    // shares almost all of its other pivots with it (at C2 the levels narrower than 1024 rows hold
+    // 99.5 % of the update pairs).
+    //   B200LU_BATCH_TAIL_MODE=1 (default): bfactor_block_kernel, kBlockRows consecutive rows per warp
+    //           sharing each loaded pivot row. Measured at C2 x 256, factor phase: 2-row blocks 25.8 ms
+    //           against 28.9 ms unsplit (tail_width 512..4096 alike; 27 ms with every row in a block);
+    //           4-row blocks cut the DRAM traffic of the trailing part 4x but run at 16 warps per SM and
+    //           wait on chain hand-offs: 32-34 ms.
+    //   B200LU_BATCH_TAIL_MODE=0: the row-by-row kernel instantiated for latency (24 loads per lane in
+    //           flight, 16 warps per SM): 34-37 ms.
+    //   B200LU_BATCH_TAIL_WIDTH=0: no split.
     const char* e = std::getenv("B200LU_BATCH_TAIL_WIDTH");
-    const int64_t tail_width = e ? std::atoll(e) : 0;
+    const int64_t tail_width = e ? std::atoll(e) : 1024;
     e = std::getenv("B200LU_BATCH_TAIL_MODE");
-    const int tail_mode = e ? std::atoi(e) : 0;
+    const int tail_mode = e ? std::atoi(e) : 1;
     const int64_t levels = static_cast<int64_t>(S.lower_width.size());
     int64_t cut = levels;
     for (int64_t l = levels - 1; l >= 1 && S.lower_width[l] < tail_width; --l) cut = l;
@@ -870,6 +872,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       BlockMeta bm;
       const int rows_here = static_cast<int>(std::min<size_t>(kBlockRows, tail_rows.size() - b0));
       std::vector<std::pair<int32_t, int>> piv;  // (pivot row, block row)
+      for (int r = 0; r < 4; ++r) bm.row[r] = -1;
       for (int r = 0; r < kBlockRows; ++r) {
         bm.row[r] = r < rows_here ? tail_rows[b0 + r] : -1;
         if (r < rows_here) {

@@ -350,16 +350,17 @@ bfactor_kernel(const BFactorArgs a) {
 // the block that has the pivot (each with its own alpha and its own destination slice), which
 // divides the re-reads of the trailing pivot rows — the dominant DRAM traffic of the unblocked
 // kernel — by the block height, and turns most chain hand-offs into program order inside one warp.
-// EXPERIMENTAL, off by default (B200LU_BATCH_TAIL_WIDTH): with blocks of consecutive row indices it
-// measures 32-34 ms against 28.9 ms unblocked at C2 x 256 (batch.cu).
-// Per row the pivots are still applied in ascending order with the same two roundings, so the
-// values stay bit-identical. A block row is published as soon as its last pivot has been applied
-// (the host marks that merge position); a pivot that is a row of the same block then finds its
-// flag already set.
-constexpr int kBlockRows = 4;
+// Block height: 2 rows per warp (80 registers, 24 warps per SM) measures 25.8 ms against 28.9 ms
+// unblocked at C2 x 256; 4 rows per warp (-DB200LU_BLOCK_ROWS=4: 126 registers, 16 warps per SM) cuts
+// the DRAM traffic of the trailing part 4x but waits on the chain hand-offs: 32-34 ms.
+#ifndef B200LU_BLOCK_ROWS
+#define B200LU_BLOCK_ROWS 2
+#endif
+constexpr int kBlockRows = B200LU_BLOCK_ROWS;  // 2 or 4
+static_assert(kBlockRows == 2 || kBlockRows == 4, "block height");
 
-struct BlockMeta {        // one 32-byte record per block
-  int32_t row[kBlockRows];  // row ids, ascending; -1 pads a short last block
+struct BlockMeta {          // one 32-byte record per block
+  int32_t row[4];           // row ids, ascending; -1 pads (short last block, kBlockRows == 2)
   int32_t mbeg, mend;       // its merged pivots
   int32_t pad0, pad1;
 };
@@ -387,7 +388,7 @@ struct BBlockArgs {
 };
 
 template <typename DestT, int S>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, kBlockRows == 2 ? 3 : 2)
 bfactor_block_kernel(const BBlockArgs a) {
   constexpr int E = 32 / S;
   constexpr int R = kBlockRows;
@@ -406,7 +407,10 @@ bfactor_block_kernel(const BBlockArgs a) {
     const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units);
     const int4 b0 = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
     const int4 b1 = __ldg(reinterpret_cast<const int4*>(a.blocks + b) + 1);
-    const int32_t rows[R] = {b0.x, b0.y, b0.z, b0.w};
+    const int32_t rows4[4] = {b0.x, b0.y, b0.z, b0.w};
+    int32_t rows[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = rows4[r];
     const int32_t mbeg = b1.x, mend = b1.y;
     const int32_t sc0 = u * S;
     double* gbase = a.values + static_cast<int64_t>(sc0 >> 5) * a.nnz_factors * 32 + (sc0 & 31) + s;

@@ -98,17 +98,18 @@ def test_batch_one_by_one_matrix():
 
 
 @needs_ref
-@pytest.mark.parametrize("mode", [1, 0])
-def test_batch_split_trailing_part(mode, monkeypatch):
-    """The optional second launch for the narrow trailing levels: mode 1 = row blocks (kBlockRows rows
-    per warp), mode 0 = the row kernel instantiated for latency."""
-    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "64")
+@pytest.mark.parametrize("width,mode", [(64, 1), (64, 0), (0, 0), (100000, 1)])
+def test_batch_trailing_part_variants(width, mode, monkeypatch):
+    """The second launch for the narrow trailing levels: mode 1 = row blocks (the default, with
+    tail width 1024), mode 0 = the row kernel instantiated for latency, width 0 = no split."""
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", str(width))
     monkeypatch.setenv("B200LU_BATCH_TAIL_MODE", str(mode))
     fx = kkt_fixture(700, 300, num_systems=4)
     f = BatchedFactors(fx.sym, 17)
     info = f.info
     f.close()
-    assert info["unit_scenarios"] == 32 and info["blocked_rows"] > 0 and (info["blocks"] > 0) == (mode == 1)
+    assert info["unit_scenarios"] == 32
+    assert (info["blocked_rows"] > 0) == (width > 0) and (info["blocks"] > 0) == (width > 0 and mode == 1)
     _check_batch(fx, 17, refine=False)
 
 
