@@ -13,6 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 tail -3 gpurun_out/ncu_bench.log
 # full captures, after warm-up
 ncu --set full --clock-control none --import-source on -k regex:bfactor_kernel -s 3 -c 1 -o gpurun_out/prof_bfactor python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-single > gpurun_out/ncu_factor.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:bfactor_block_kernel -s 3 -c 1 -o gpurun_out/prof_bblock python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-single >> gpurun_out/ncu_factor.log 2>&1
 tail -3 gpurun_out/ncu_factor.log
 ncu --set full --clock-control none --import-source on -k regex:btri_kernel -s 18 -c 3 -o gpurun_out/prof_btri python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-single > gpurun_out/ncu_tri.log 2>&1
 ls -la gpurun_out

@@ -83,8 +83,9 @@ def main():
     for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         md.append(f"| `{k.strip()[:70]}` | {c} | {t:.1f} | {t / tot:.3f} | {t / c:.1f} |")
     traffic = {}
+    seen = set()
     for rep in reps:
-        for kr in ("factor_kernel", "tri_kernel", "tail_kernel"):
+        for kr in ("factor_kernel", "factor_block_kernel", "tri_kernel", "tail_kernel"):
             ms = raw_metrics(rep, kr)
             if not ms:
                 continue
@@ -94,12 +95,15 @@ def main():
                 for w in WANT:
                     if w in m:
                         md.append(f"  * {w} = {m[w][0]} {m[w][1]}")
-                if kr == "factor_kernel" and "dram__bytes_read.sum" in m and "factor_kernel_dram_bytes" not in traffic:
+                if kr in ("factor_kernel", "factor_block_kernel") and "dram__bytes_read.sum" in m and kr not in seen:
+                    # one refactorization = the head launch + the row-blocked trailing launch: their traffic adds up
+                    seen.add(kr)
                     def mb(x):
                         v, u = x
                         v = float(v.replace(",", ""))
                         return v * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[u]
-                    traffic["factor_kernel_dram_bytes"] = mb(m["dram__bytes_read.sum"]) + mb(m["dram__bytes_write.sum"])
+                    traffic["factor_kernel_dram_bytes"] = traffic.get("factor_kernel_dram_bytes", 0.0) + \
+                        mb(m["dram__bytes_read.sum"]) + mb(m["dram__bytes_write.sum"])
             try:
                 tot_s, stalls, lines = source_top(rep, kr)
                 md += ["", f"Stall samples ({tot_s} total): " + ", ".join(f"{k}={v}" for k, v in stalls), "",
