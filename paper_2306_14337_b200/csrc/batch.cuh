@@ -387,12 +387,19 @@ struct BBlockArgs {
   unsigned long long* ticket;
 };
 
+#ifndef B200LU_BLOCK_MINB
+#define B200LU_BLOCK_MINB (kBlockRows == 2 ? 3 : 2)
+#endif
 template <typename DestT, int S>
-__global__ void __launch_bounds__(256, kBlockRows == 2 ? 3 : 2)
+__global__ void __launch_bounds__(256, B200LU_BLOCK_MINB)
 bfactor_block_kernel(const BBlockArgs a) {
   constexpr int E = 32 / S;
   constexpr int R = kBlockRows;
+#ifdef B200LU_BLOCK_UNROLL
+  constexpr int kUnroll = B200LU_BLOCK_UNROLL;
+#else
   constexpr int kUnroll = 8;
+#endif
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int s = lane % S, e = lane / S;
