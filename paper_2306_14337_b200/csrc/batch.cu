@@ -99,6 +99,8 @@ struct b200lu_batch {
 
   void (*factor_fn)(BFactorArgs) = nullptr;
   int factor_grid = 0, tri_grid = 0, tri_grid_upper = 0, tri_grid_chain = 0;
+  void (*chain_fn)(BTriArgs) = nullptr;  // U sweep, narrow leading levels
+  int chain_warps = 8, chain_buf = kTriBufferedChain;
   int32_t upper_chain_rows = 0;  // leading rows of the U level order handled by the chain launch
   size_t factor_smem = 0;
 
@@ -377,7 +379,7 @@ b200lu_status launch_upper(H* h, const double* y, double* x) {
   BTriArgs a = tri_args(h, h->d_upper_meta, y, x, 2);
   if (h->upper_chain_rows > 0) {  // the narrow leading levels: whole rows parked, one CTA per SM
     a.count = h->upper_chain_rows;
-    btri_kernel<true, kTriBufferedChain><<<h->tri_grid_chain, 256, tri_upper_smem(kTriBufferedChain), h->stream>>>(a);
+    h->chain_fn<<<h->tri_grid_chain, h->chain_warps * 32, tri_upper_smem(h->chain_buf, h->chain_warps), h->stream>>>(a);
     ST_TRY(check_launch(h, "btri_kernel<upper chain>"));
   }
   if (h->upper_chain_rows < h->n) {
@@ -1070,13 +1072,25 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     int o1 = 0, o2 = 0, o3 = 0;
     CU_TRY(h, cudaFuncSetAttribute(btri_kernel<true, kTriBufferedWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(tri_upper_smem(kTriBufferedWide))));
-    CU_TRY(h, cudaFuncSetAttribute(btri_kernel<true, kTriBufferedChain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(tri_upper_smem(kTriBufferedChain))));
+    {
+      // experiments: buffer entries and warps per CTA of the chain launch (B200LU_BATCH_UBUF / _UWARPS)
+      const char* eb = std::getenv("B200LU_BATCH_UBUF");
+      const char* ew = std::getenv("B200LU_BATCH_UWARPS");
+      // measured at C2 x 256 (per U sweep): 96 entries x 8 warps/SM 2.77 ms, 64 x 12 warps/SM 2.25 ms,
+      // 48 x 16 warps/SM 2.97 ms (rows longer than the buffer pay a memory round trip per extra chunk)
+      const int ub = eb ? std::atoi(eb) : 64;
+      h->chain_warps = ew && std::atoi(ew) == 8 ? 8 : 4;
+      h->chain_buf = ub == 48 ? 48 : ub == 96 ? kTriBufferedChain : 64;
+      h->chain_fn = h->chain_buf == 48 ? btri_kernel<true, 48> : h->chain_buf == 64 ? btri_kernel<true, 64>
+                                                                                     : btri_kernel<true, kTriBufferedChain>;
+    }
+    CU_TRY(h, cudaFuncSetAttribute(h->chain_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(tri_upper_smem(h->chain_buf, h->chain_warps))));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, btri_kernel<false, kTriBufferedWide>, 256, 0));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, btri_kernel<true, kTriBufferedWide>, 256,
                                                             tri_upper_smem(kTriBufferedWide)));
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, btri_kernel<true, kTriBufferedChain>, 256,
-                                                            tri_upper_smem(kTriBufferedChain)));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, h->chain_fn, h->chain_warps * 32,
+                                                            tri_upper_smem(h->chain_buf, h->chain_warps)));
     h->tri_grid = prop.multiProcessorCount * std::max(1, o1);
     h->tri_grid_upper = prop.multiProcessorCount * std::max(1, o2);
     h->tri_grid_chain = prop.multiProcessorCount * std::max(1, o3);

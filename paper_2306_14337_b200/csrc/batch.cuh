@@ -569,7 +569,7 @@ struct BTriArgs {
 // occupancy.
 constexpr int kTriChunk = 8;
 constexpr int kTriBufferedWide = 32, kTriBufferedChain = 96;
-constexpr size_t tri_upper_smem(int buffered) { return static_cast<size_t>(8) * buffered * 32 * sizeof(double); }
+constexpr size_t tri_upper_smem(int buffered, int warps = 8) { return static_cast<size_t>(warps) * buffered * 32 * sizeof(double); }
 
 template <bool kUpper, int kTriBuffered>
 __global__ void __launch_bounds__(256)
