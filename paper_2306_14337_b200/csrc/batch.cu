@@ -73,6 +73,7 @@ struct b200lu_batch {
   int64_t blocked_pairs = 0;
   void (*block_fn)(BBlockArgs) = nullptr;
   int block_grid = 0;
+  size_t block_smem = 0;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
@@ -324,7 +325,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       bb.pivot_floor = h->pivot_floor;
       bb.failed = h->d_failed;
       bb.ticket = h->d_tickets + 1;
-      h->block_fn<<<h->block_grid, 256, 0, h->stream>>>(bb);
+      h->block_fn<<<h->block_grid, 256, h->block_smem, h->stream>>>(bb);
       ST_TRY(check_launch(h, "bfactor_block_kernel"));
     }
   }
@@ -892,6 +893,11 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
         last_of_row[piv[q].second] = static_cast<int>(merged.size()) - 1;
       }
       for (int r = 0; r < rows_here; ++r) merged[last_of_row[r]].bits |= 256u << r;
+      for (int32_t t = bm.mbeg; t < static_cast<int32_t>(merged.size()); ++t) {
+        for (int r = 0; r < rows_here; ++r) {
+          if (merged[t].d == bm.row[r]) merged[t].bits |= 0x10000u;  // a pivot that is a row of this block
+        }
+      }
       bm.mend = static_cast<int32_t>(merged.size());
       bm.pad0 = bm.pad1 = 0;
       blocks.push_back(bm);
@@ -1064,8 +1070,12 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     using BFn = void (*)(BBlockArgs);
     BFn bfn = h->dest16 ? bfactor_block_kernel<uint16_t, 32> : bfactor_block_kernel<uint32_t, 32>;
     h->block_fn = bfn;
+    h->block_smem = 8 * block_stage_doubles() * sizeof(double);
+    if (h->block_smem > 0) {
+      CU_TRY(h, cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->block_smem)));
+    }
     int bocc = 0;
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, 0));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, h->block_smem));
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
   }
   {
