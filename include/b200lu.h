@@ -264,7 +264,7 @@ typedef struct b200lu_batch b200lu_batch;
 
 typedef struct {
   int64_t batch, padded_batch;
-  int64_t unit_scenarios; /* scenarios a refactorization warp handles at once (8, 16 or 32) */
+  int64_t unit_scenarios; /* scenarios a refactorization warp handles at once: 32, one lane per scenario */
   int64_t blocks;         /* row blocks of the trailing part of the refactorization (kBlockRows rows each) */
   int64_t factor_rows;    /* rows with at least one pivot */
   int64_t blocked_rows, blocked_pairs; /* of those, rows (and their update pairs) handled in row blocks */
