@@ -23,9 +23,12 @@ host-side symbolic analysis, produced once before the timed region through the r
           memory and x copied D2H inside the timed region, every step.
   --impl reference   the unmodified reference CPU implementation (oracle/_ref) on this box's cores.
 
-Under torchrun every rank runs the same workload on its own scenarios (same pattern, different
-values) — weak scaling with no data-path collective; NCCL/gloo only carries the per-rank timings,
-residuals and per-system records to rank 0.
+Multi-GPU (BASELINE config 5: "batch of 256 ... sharded over 1/2/4/8 B200"): `--gpus N` shards the
+`--scenarios` (256) scenarios of the batch over the N ranks in contiguous blocks — 256/N per GPU, the
+total fixed: STRONG scaling — with no data-path collective; NCCL only carries the per-rank timings,
+residuals and per-system records to rank 0. `--scenarios-per-gpu S` fixes the per-GPU batch instead
+(weak scaling line). Without a launcher (`WORLD_SIZE` unset) and N > 1 the script re-executes itself
+under `python -m torch.distributed.run --nproc-per-node N` on 127.0.0.1.
 """
 from __future__ import annotations
 
@@ -80,6 +83,21 @@ def batch_algorithmic_bytes(batch, n, nnz_a, nnz_f, fgmres_iters=1):
                 total=scatter + eliminate + solve + fgmres)
 
 
+def recorded_traffic(key):
+    """DRAM bytes per launch of the dominant kernel. NOT measured in this run (a bench value is never
+    taken under a profiler): the figure is the one recorded by the last `ncu --set full` capture of the
+    same command (tools/gpu_bench_profile.sh writes profiles/traffic.json), and the line says so."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return None, "none recorded"
+    rec = json.load(open(tp)).get(key, {})
+    if "factor_kernel_dram_bytes" not in rec:
+        return None, "none recorded for this workload"
+    return rec["factor_kernel_dram_bytes"], ("recorded constant from " + rec.get("source", "profiles/traffic.json") +
+                                             " (ncu --set full capture, dram__bytes_read.sum + dram__bytes_write.sum); "
+                                             "not re-measured in this run")
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -128,6 +146,22 @@ class ClockSampler:
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def nccl_init_lines():
+    """The communicator lines NCCL logged at init (NCCL_DEBUG=INFO, subsystem INIT, into
+    NCCL_DEBUG_FILE — set in run_b200): rank count, transport, NVLS, so the reader can check that the N
+    ranks really formed one communicator."""
+    path = os.environ.get("B200LU_NCCL_LOG")
+    if not path or not os.path.exists(path):
+        return []
+    keep = []
+    for ln in open(path, errors="replace"):
+        if any(k in ln for k in ("nranks", "Init COMPLETE", "NVLS", "Connected all", "via P2P", "NET/")):
+            keep.append(ln.strip()[:240])
+    for ln in keep[:12]:
+        print("[nccl] " + ln, file=sys.stderr)
+    return keep[:12]
 
 
 def dist_env():
@@ -316,10 +350,7 @@ def measure_single(args, workload, steps, with_cpu_baseline):
     fac_ms, fac_n = phases["factor"]
     fac_avg_ms = fac_ms / max(fac_n, 1)
     achieved = ab["eliminate"] / (fac_avg_ms * 1e-3) / 1e9 if fac_avg_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(workload, {}).get("factor_kernel_dram_bytes")
+    traffic, traffic_src = recorded_traffic(workload)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -346,7 +377,7 @@ def measure_single(args, workload, steps, with_cpu_baseline):
         "roofline": {
             "kernel": "factor_kernel (K2 numeric refactorization)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
-            "traffic": traffic, "peak_source": peak_src,
+            "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
             "bytes_model": "SURVEY 8(d): eliminate = 20*nnz(L+U) + 8*N per system, one system per launch",
             "whole_step": {"algorithmic_bytes": ab["total"],
@@ -431,10 +462,16 @@ def run_batch(args):
     from oracle import refbridge as rb  # input fixtures + CPU baseline arm only
 
     rank, local_rank, world = dist_env()
-    S = args.scenarios
     n, m, desc = WORKLOADS["C2"]
-    total_scen = S * world
+    if args.scenarios_per_gpu > 0:   # weak line: fixed batch per GPU
+        total_scen, scaling = args.scenarios_per_gpu * world, "weak"
+    else:                            # BASELINE config 5: the batch is sharded, its size is fixed
+        total_scen, scaling = args.scenarios, "strong"
     mine = scenario_assignment(total_scen, world, rank)
+    S = len(mine)
+    if S == 0:
+        raise SystemExit(f"bench.py: {total_scen} scenarios cannot be sharded over {world} ranks")
+    S_max = -(-total_scen // world)
     # ---- input fixture (untimed): one generated scenario per y_seed, one symbolic analysis
     seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1, keep_blocks=True) for sc in mine]
     ref_sym = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
@@ -544,10 +581,14 @@ def run_batch(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max, e2e_ms_max, relres_max, kkt_ms_max = (float(v) for v in t.cpu())
 
-    single = None
-    if not args.no_single:
+    # the single-system measurements ride on the N = 1 line only (they do not shard)
+    single = c4 = None
+    if not args.no_single and world == 1:
         single = measure_single(args, args.single_workload, min(args.steps * 2, 20), False)
+        if not args.no_c4:
+            c4 = measure_single(args, "C4", min(args.steps, 10), False)
 
+    nccl_lines = nccl_init_lines() if world > 1 else None
     if rank == 0:
         ms_per_step = total_ms_max / args.steps
         value = total_scen * args.steps / (total_ms_max / 1000.0)
@@ -558,21 +599,19 @@ def run_batch(args):
         fac_ms, fac_n = phases["factor"]
         fac_avg_ms = fac_ms / max(fac_n, 1)
         achieved = ab["eliminate"] / (fac_avg_ms * 1e-3) / 1e9 if fac_avg_ms > 0 else 0.0
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(f"C5x{S}", {}).get("factor_kernel_dram_bytes")
+        traffic, traffic_src = recorded_traffic(f"C5x{S}")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": f"C5: batch of {S} independent scenario systems per GPU ({total_scen} in total), each "
+                "workload": f"C5: batch of {total_scen} independent scenario systems sharded over {world} GPU(s) in "
+                            f"contiguous blocks ({S_max} per GPU), each "
                             f"{desc} (C2-shaped), one shared pattern / symbolic analysis, y_seed = 2 + scenario; one "
                             f"step = the whole batch through scatter + refactorize + solve_system"
                             f"{'' if args.no_refine else ' + fgmres_refine(tol=%g)' % args.refine_tol} with the "
                             "interleaved scenario-batch kernels; gen_sequence defaults, AMD-only analysis (KLU-style path)",
-                "scenarios_per_gpu": S, "n": N, "nnz": nnz_a, "nnz_factors": nnz_f,
+                "scenarios_total": total_scen, "scenarios_per_gpu": S_max, "n": N, "nnz": nnz_a, "nnz_factors": nnz_f,
                 "update_pairs": info["update_pairs"], "levels": info["lower_levels"],
                 "unit_scenarios": info["unit_scenarios"], "device_gb": round(info["device_bytes"] / 1e9, 2),
                 "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); the "
@@ -580,15 +619,15 @@ def run_batch(args):
                 "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks",
             },
             "clocks": clocks,
-            "ms_per_system": ms_per_step / S,
+            "ms_per_system": ms_per_step / total_scen,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms_max / args.steps,
-                    "h2d_bytes_per_step": 8 * S * (nnz_a + N), "d2h_bytes_per_step": 8 * S * N,
+                    "h2d_bytes_per_step": 8 * total_scen * (nnz_a + N), "d2h_bytes_per_step": 8 * total_scen * N,
                     "note": "values + rhs of every scenario from pinned host memory H2D and every x D2H inside the "
                             "timed region, through the public BatchedFactors refactorize/solve_system/fgmres_refine calls"},
             "e2e_kkt_diagonal": {
                 "value": total_scen * args.steps / (kkt_ms_max / 1000.0), "unit": UNIT,
-                "ms_per_step": kkt_ms_max / args.steps, "h2d_bytes_per_step": 8 * S * (n + N),
-                "d2h_bytes_per_step": 8 * S * N, "bitwise_equal_to_full_value_submission": kkt_same,
+                "ms_per_step": kkt_ms_max / args.steps, "h2d_bytes_per_step": 8 * total_scen * (n + N),
+                "d2h_bytes_per_step": 8 * total_scen * N, "bitwise_equal_to_full_value_submission": kkt_same,
                 "note": "same step submitted through the device-resident KKT value path (b200lu_batch_kkt_update, "
                         "SURVEY 8f-1): the scenarios share H and J, so only each scenario's barrier diagonal D_y "
                         "(n_primal doubles) and rhs are copied H2D and K's diagonal is rewritten on the device"},
@@ -604,7 +643,7 @@ def run_batch(args):
             "roofline": {
                 "kernel": "bfactor_kernel + bfactor_block_kernel (K2 numeric refactorization, scenario-batched: head launch + row-blocked trailing launch, timed as one)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
-                "traffic": traffic, "peak_source": peak_src,
+                "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
                 "bytes_model": f"SURVEY 8(d) C5 row: eliminate = {S} scenarios x 16*nnz(L+U) value bytes + one copy of "
                                "the int32 indices (4*nnz(L+U) + 8*N), all scenarios in one launch",
@@ -617,11 +656,15 @@ def run_batch(args):
                                 "all scenarios of the batch",
             },
         }
+        keys = ("value", "unit", "ms_per_step", "config", "e2e", "phases_ms_per_step", "refine_iters_median",
+                "relres_final_max", "roofline", "gpu_launches")
         if single is not None:
-            line["single_system"] = {k: single[k] for k in ("value", "unit", "ms_per_step", "config", "e2e",
-                                                            "phases_ms_per_step", "refine_iters_median",
-                                                            "relres_final_max", "roofline", "gpu_launches")}
-        if world == 1 and not args.no_cpu_baseline:
+            line["single_system"] = {k: single[k] for k in keys}
+        if c4 is not None:
+            line["c4"] = {k: c4[k] for k in keys}
+        if nccl_lines is not None:
+            line["nccl"] = nccl_lines
+        if not args.no_cpu_baseline:  # rank 0, at every N: the reference on this box's host cores
             threads = rb.max_threads()
             sample = min(S, threads * max(1, args.cpu_reps // 2))
             rate, how, cal, worst = reference_batch_best(rb, ref_sym, seqs[:sample], threads, not args.no_refine,
@@ -632,6 +675,7 @@ def run_batch(args):
                 "calibration": cal, "worst_relres_final": worst}
         print(json.dumps(line))
     if world > 1:
+        dist.barrier()  # the other ranks wait for rank 0's CPU baseline before tearing the group down
         dist.destroy_process_group()
 
 
@@ -675,7 +719,7 @@ def run_reference_batch(args):
               f"; {threads} host threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C5: independent scenario systems, each {desc} (C2-shaped), shared pattern; "
                                "scatter+eliminate+solve_system+fgmres_refine per system (cli.cpp:105-135); reference CPU path",
@@ -710,6 +754,9 @@ def run_b200(args):
         if one_device:
             dist.init_process_group("gloo")
         else:
+            if "NCCL_DEBUG" not in os.environ:  # rank lines for the record, kept out of stdout (one JSON line only)
+                log = os.path.join(tempfile.gettempdir(), f"b200lu_nccl_{os.getpid()}.log")
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE=log, B200LU_NCCL_LOG=log)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.workload == BATCH_WORKLOAD:
         run_batch(args)
@@ -728,7 +775,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default=BATCH_WORKLOAD, choices=sorted(WORKLOADS) + [BATCH_WORKLOAD])
-    ap.add_argument("--scenarios", type=int, default=256, help="C5: scenarios per GPU")
+    ap.add_argument("--scenarios", type=int, default=256, help="C5: scenarios of the batch in TOTAL, sharded over the GPUs")
+    ap.add_argument("--scenarios-per-gpu", type=int, default=0, help="C5: fix the per-GPU batch instead (weak scaling)")
+    ap.add_argument("--no-c4", action="store_true", help="C5: skip the C4 (n = 1.6 M) single-system block")
     ap.add_argument("--single-workload", default="C3", choices=sorted(WORKLOADS),
                     help="C5: the single-system measurement reported next to the batch")
     ap.add_argument("--no-single", action="store_true", help="C5: skip the single-system measurement")
@@ -739,6 +788,15 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # self-launch: one rank per GPU on this node (rendezvous on 127.0.0.1: the hostname may not resolve)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         (run_reference_batch if args.workload == BATCH_WORKLOAD else run_reference)(args)
     else:

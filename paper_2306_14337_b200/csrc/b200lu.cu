@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kFactorWarps = 8;
 constexpr int kMaxBigSlot = 20 * 1024; // doubles; wider rows fall back to in-place global updates
+constexpr int kMaxTailRows = 24576;     // rows of an on-chip tail (ScheduleTuning::tail_capacity is capped to this)
 constexpr int kReduceBlocks = 592;     // 4 per SM on a 148-SM part; fixed so sums are reproducible
 
 __global__ void arm_factor_kernel(int32_t* counters, int32_t* failed_row) {
@@ -326,7 +327,7 @@ b200lu_status launch_lower(H* h, const double* y, double* x) {
     if (h->concurrency > 1) {  // static claim order needs the whole grid resident
       tri_kernel<false, false, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
     } else {
-      tri_kernel<false, false, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+      CU_TRY(h, launch_resident(tri_kernel<false, false, true>, h->tri_grid, 256, 0, h->stream, a));
     }
     ST_TRY(check_launch(h, "tri_kernel<lower head>"));
     init = h->d_partial;
@@ -360,7 +361,7 @@ b200lu_status launch_upper(H* h, const double* y, double* x) {
     if (h->concurrency > 1) {
       tri_kernel<true, true, false><<<h->tri_grid, 256, 0, h->stream>>>(a);
     } else {
-      tri_kernel<true, true, true><<<h->tri_grid, 256, 0, h->stream>>>(a);
+      CU_TRY(h, launch_resident(tri_kernel<true, true, true>, h->tri_grid, 256, 0, h->stream, a));
     }
     ST_TRY(check_launch(h, "tri_kernel<upper head>"));
   }
@@ -769,7 +770,7 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   if (const char* e = std::getenv("B200LU_SOLVE_MIN_WINDOW")) h->tune.solve_min_window = std::atoll(e);
   if (const char* e = std::getenv("B200LU_SOLVE_MAX_WINDOW")) h->tune.solve_max_window = std::atoll(e);
   if (const char* e = std::getenv("B200LU_TAIL_WIDTH")) h->tune.tail_width = std::atoll(e);
-  if (const char* e = std::getenv("B200LU_TAIL_CAPACITY")) h->tune.tail_capacity = std::min<int64_t>(std::atoll(e), 24576);
+  if (const char* e = std::getenv("B200LU_TAIL_CAPACITY")) h->tune.tail_capacity = std::min<int64_t>(std::atoll(e), kMaxTailRows);
   const std::string err = build_schedule(*sym, h->tune, h->sched);
   if (!err.empty()) {
     h->last_error = err;
@@ -814,8 +815,11 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
     ST_TRY(upload_tail(S.lower_tail, h->lower_tail));
     ST_TRY(upload_tail(S.upper_tail, h->upper_tail));
     ST_TRY(dev_alloc(h, &h->d_partial, n));
-    const int tail_smem = static_cast<int>(std::max(S.lower_tail.rows, S.upper_tail.rows) * sizeof(double));
-    if (tail_smem > 0) {
+    // The attribute is per FUNCTION and process-wide, not per handle: it is set to the fixed upper
+    // bound (tail_capacity rows) so that a second handle with a smaller tail never lowers the limit
+    // under a live one.
+    if (S.lower_tail.rows > 0 || S.upper_tail.rows > 0) {
+      const int tail_smem = static_cast<int>(kMaxTailRows * sizeof(double));
       CU_TRY(h, cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem));
       CU_TRY(h, cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem));
     }
@@ -950,8 +954,9 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
     h->factor_fn = h->dest16 ? f16[v] : f32[v];
   }
   int occ = 0;
+  // per function, process-wide: always the fixed upper bound (see the tail kernels above)
   CU_TRY(h, cudaFuncSetAttribute(h->factor_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(h->factor_smem)));
+                                 static_cast<int>((static_cast<size_t>(kFactorWarps) * h->tune.small_slot + kMaxBigSlot) * sizeof(double))));
   CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->factor_fn, kFactorWarps * 32, h->factor_smem));
   if (occ < 1) {
     h->last_error = "factor kernel does not fit on an SM";

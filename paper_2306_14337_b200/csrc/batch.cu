@@ -371,7 +371,8 @@ b200lu_status arm_solve(H* h) {
 
 b200lu_status launch_lower(H* h, const double* y, double* x) {
   PhaseScope ps(h, B200LU_PHASE_LOWER);
-  btri_kernel<false, kTriBufferedWide><<<h->tri_grid, 256, 0, h->stream>>>(tri_args(h, h->d_lower_meta, y, x, 1));
+  // static claim order: the grid must be co-resident (launch_resident, common.cuh)
+  CU_TRY(h, launch_resident(btri_kernel<false, kTriBufferedWide>, h->tri_grid, 256, 0, h->stream, tri_args(h, h->d_lower_meta, y, x, 1)));
   return check_launch(h, "btri_kernel<lower>");
 }
 
@@ -380,14 +381,14 @@ b200lu_status launch_upper(H* h, const double* y, double* x) {
   BTriArgs a = tri_args(h, h->d_upper_meta, y, x, 2);
   if (h->upper_chain_rows > 0) {  // the narrow leading levels: whole rows parked, one CTA per SM
     a.count = h->upper_chain_rows;
-    h->chain_fn<<<h->tri_grid_chain, h->chain_warps * 32, tri_upper_smem(h->chain_buf, h->chain_warps), h->stream>>>(a);
+    CU_TRY(h, launch_resident(h->chain_fn, h->tri_grid_chain, h->chain_warps * 32, tri_upper_smem(h->chain_buf, h->chain_warps), h->stream, a));
     ST_TRY(check_launch(h, "btri_kernel<upper chain>"));
   }
   if (h->upper_chain_rows < h->n) {
     a.first = h->upper_chain_rows;
     a.count = static_cast<int32_t>(h->n) - h->upper_chain_rows;
     a.ticket = h->d_tickets + 3;
-    btri_kernel<true, kTriBufferedWide><<<h->tri_grid_upper, 256, tri_upper_smem(kTriBufferedWide), h->stream>>>(a);
+    CU_TRY(h, launch_resident(btri_kernel<true, kTriBufferedWide>, h->tri_grid_upper, 256, tri_upper_smem(kTriBufferedWide), h->stream, a));
     ST_TRY(check_launch(h, "btri_kernel<upper wide>"));
   }
   return B200LU_OK;

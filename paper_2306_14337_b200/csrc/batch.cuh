@@ -21,12 +21,14 @@ namespace b200lu {
 
 constexpr int kBatchLanes = 32;
 
-// Flag load. Relaxed at gpu scope (served by L2, no L1 invalidation): the data it guards is read
-// afterwards with L2-only accesses (ld.global.cg / cp.async.cg) that depend on the flag's value,
-// and the producer fences between its data stores and the flag store.
+// Flag load with ACQUIRE semantics at gpu scope: the data it guards (another SM's stores, fenced and
+// then flagged with a relaxed store, i.e. a release pattern) is read afterwards with ordinary L2-only
+// loads / asynchronous copies, and the PTX memory model orders those behind the flag only through an
+// acquire — a control dependency on a relaxed load is not enough on paper, whatever the hardware did
+// in the stress runs.
 __device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 // Spins until the (row, unit) flag reaches `gen`. The poll is paced (sleep doubling from 32 ns to

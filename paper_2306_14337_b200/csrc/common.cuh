@@ -105,4 +105,16 @@ __device__ __forceinline__ double add_prod(double a, double b, double c) {
   return __dadd_rn(a, __dmul_rn(b, c));
 }
 
+// Launch of a kernel whose claim order is STATIC (warp w takes units w, w + W, ...): such a kernel is
+// deadlock-free only when its whole grid is co-resident, because the owner of the lowest unfinished
+// unit must be running. A cooperative launch makes the driver guarantee exactly that — the grid is
+// scheduled as a whole, waiting for SMs if another handle's kernel (or another MPS client) occupies
+// them — and fails at launch time (cudaErrorCooperativeLaunchTooLarge) if the grid could never fit,
+// instead of hanging the device.
+template <typename Arg>
+inline cudaError_t launch_resident(void (*kernel)(Arg), int grid, int block, size_t smem, cudaStream_t stream, Arg arg) {
+  void* params[] = {&arg};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(block), params, smem, stream);
+}
+
 }  // namespace b200lu

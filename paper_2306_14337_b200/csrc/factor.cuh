@@ -37,6 +37,9 @@ scatter_kernel(int64_t nnz_factors, const int32_t* __restrict__ src_of_slot,
       if (scatter_scale != nullptr) v = __dmul_rn(v, __ldg(scatter_scale + k));
     }
     work[s] = v;
+    // a directly published value that carries the marker's bit pattern (an input NaN payload) would
+    // make every dependent row wait forever: canonicalise it, as publish() does for computed rows
+    if (trivial && is_pending(v)) v = __longlong_as_double(static_cast<long long>(kCanonicalNaN));
     values[s] = trivial ? v : pending;
   }
 }

@@ -273,15 +273,10 @@ def _values_ptr(A: CsrMatrix):
 
 
 def _guard_pattern(f: NumericFactors, A: CsrMatrix):
-    """scatter_values' guards, src/numeric.cpp:15-18. The element-wise pattern comparison
-    (pattern_equal) is done once per (matrix object, handle): a CsrMatrix whose pattern arrays
-    were verified against this handle is trusted afterwards, so a sequence that re-submits the
-    same pattern arrays with new values pays the 8*(n+1+nnz)-byte comparison only once."""
-    if not A.has_values():
-        if getattr(A, "_verified_for", None) == id(f):
-            raise Error("scatter_values: matrix has no values")
-    if getattr(A, "_verified_for", None) == id(f) and A.has_values():
-        return
+    """scatter_values' guards, src/numeric.cpp:15-18: pattern_equal runs on EVERY scatter, as in
+    the reference — an 8*(n+1+nnz)-byte memcmp, small next to a factorization — so neither a
+    recycled handle nor an in-place edit of the pattern arrays can slip through. The value count is
+    checked too: reset_values copies nnz_source doubles from the caller's buffer."""
     ro, ci = _i64(A.row_offsets), _i64(A.col_indices)
     st = _capi.PATTERN_MISMATCH
     if A.nrows == A.ncols and ro.size == A.nrows + 1 and ci.size == len(f.symbolic.src_col_indices):
@@ -290,10 +285,9 @@ def _guard_pattern(f: NumericFactors, A: CsrMatrix):
         raise PatternMismatchError("matrix pattern differs from the analyzed pattern")
     if not A.has_values():
         raise Error("scatter_values: matrix has no values")
-    try:
-        A._verified_for = id(f)
-    except Exception:
-        pass
+    nvals = A.values.numel() if _is_device_tensor(A.values) else np.asarray(A.values).size
+    if nvals != ci.size:
+        raise PatternMismatchError("matrix has %d values for %d pattern entries" % (nvals, ci.size))
 
 
 def reset_values(f: NumericFactors, A: CsrMatrix):
