@@ -271,6 +271,11 @@ typedef struct {
   int64_t factor_grid, tri_grid;
   int64_t n, nnz_factors, nnz_source, update_pairs, lower_levels, upper_levels;
   int64_t device_bytes, alloc_events, launches;
+  /* tiled trailing part (csrc/tile.cuh): rows resident in shared memory, pivot rows streamed by TMA */
+  int64_t tiled;                /* 1: the trailing part runs in the tiled kernel (then `blocks` counts tiles) */
+  int64_t tile_rows;            /* rows (consumer warps) per tile */
+  int64_t tile_smem_bytes, tile_grid;
+  int64_t tile_fetched_entries; /* pivot-row entries TMA fetches per 8-scenario unit (x 64 bytes) */
 } b200lu_batch_info;
 
 /* NumericFactors::NumericFactors (src/numeric.cpp:8-12) for `batch` systems at once. Only
@@ -320,6 +325,25 @@ b200lu_status b200lu_batch_kkt_bind(b200lu_batch* h, int64_t n_primal, const dou
 b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on_device, double delta_p,
                                       double delta_d);
 b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out);
+
+/* Diagnostics — HOST ONLY, needs no device; not on any product path. Builds the tile plan the batched
+ * refactorization derives for the trailing rows of the pattern (rows_per_tile rows and tile_entries
+ * row entries of shared memory per tile, trailing part = the levels narrower than tail_width rows) and
+ * executes that plan for ONE scenario on the host with the index arithmetic of the device kernel:
+ * `values` holds the scattered matrix (scatter_values, src/numeric.cpp:14-23) on entry and the factors
+ * on return; the arithmetic is eliminate's (src/numeric.cpp:34-49). The CPU tests compare the result
+ * with the oracle bit for bit, which pins the plan (tiling, pivot merge, chunking, claim order) without
+ * a GPU. Returns B200LU_ZERO_PIVOT with *failed_row as eliminate would. */
+typedef struct {
+  int64_t tiles, rows, items;
+  int64_t pairs;                /* update pairs of the tiled rows */
+  int64_t fetched_entries;      /* pivot-row entries fetched per unit (each pivot row once per tile) */
+  int64_t consumed_entries;     /* the same entries counted once per consuming row (= no sharing) */
+  int64_t largest_tile_entries;
+} b200lu_tile_plan_stats;
+b200lu_status b200lu_tile_plan_emulate(const b200lu_symbolic_view* sym, int rows_per_tile, int64_t tile_entries,
+                                       int64_t tail_width, double pivot_floor, double* values, int64_t* failed_row,
+                                       b200lu_tile_plan_stats* stats, char* error_buf, int error_buf_len);
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled);
 b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset);
 b200lu_status b200lu_batch_synchronize(b200lu_batch* h);

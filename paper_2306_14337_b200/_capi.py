@@ -48,7 +48,13 @@ class BatchInfo(C.Structure):
     _fields_ = [(k, i64) for k in ("batch", "padded_batch", "unit_scenarios", "blocks", "factor_rows",
                                    "blocked_rows", "blocked_pairs", "factor_grid", "tri_grid", "n", "nnz_factors",
                                    "nnz_source", "update_pairs", "lower_levels", "upper_levels", "device_bytes",
-                                   "alloc_events", "launches")]
+                                   "alloc_events", "launches", "tiled", "tile_rows", "tile_smem_bytes", "tile_grid",
+                                   "tile_fetched_entries")]
+
+
+class TilePlanStats(C.Structure):
+    _fields_ = [(k, i64) for k in ("tiles", "rows", "items", "pairs", "fetched_entries", "consumed_entries",
+                                   "largest_tile_entries")]
 
 
 EXPORTS = {
@@ -104,6 +110,8 @@ EXPORTS = {
     "b200lu_batch_refine_fgmres": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
     "b200lu_batch_refine_classic": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
     "b200lu_batch_get_info": (i32, [vp, C.POINTER(BatchInfo)]),
+    "b200lu_tile_plan_emulate": (i32, [C.POINTER(SymbolicView), i32, i64, i64, dbl, vp, C.POINTER(i64),
+                                       C.POINTER(TilePlanStats), C.c_char_p, i32]),
     "b200lu_batch_set_timing": (i32, [vp, i32]),
     "b200lu_batch_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
     "b200lu_batch_synchronize": (i32, [vp]),

@@ -20,6 +20,7 @@
 
 #include "batch.cuh"
 #include "schedule.hpp"
+#include "tile.cuh"
 
 using namespace b200lu;
 
@@ -74,6 +75,21 @@ struct b200lu_batch {
   void (*block_fn)(BBlockArgs) = nullptr;
   int block_grid = 0;
   size_t block_smem = 0;
+  // tiled trailing part (tile.cuh): rows resident in shared memory, pivot rows streamed by TMA
+  bool use_tiles = false;
+  std::string tile_note;          // why the tiled kernel is not used, if it is not
+  TileMeta* d_tile_meta = nullptr;
+  TileRow* d_tile_rows = nullptr;
+  ExtItem* d_tile_ext = nullptr;
+  RowItem* d_tile_row_items = nullptr;
+  uint16_t* d_tile_dest = nullptr;
+  int32_t* d_tile_flags = nullptr;  // [n][tile_units]
+  int32_t n_tiles = 0, tile_units = 0, tile_rows_per = 8;
+  int64_t tile_fetched_entries = 0;
+  void (*tile_fn)(BTileArgs) = nullptr;
+  int tile_grid = 0;
+  size_t tile_smem = 0;
+  BTileArgs tile_args;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
@@ -281,7 +297,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
         cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
     ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
   }
-  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0) {
+  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0 || h->n_tiles > 0) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
@@ -307,6 +323,13 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       a.ticket = h->d_tickets + 1;
       h->tail_fn<<<h->tail_grid, kBWarps * 32, 0, h->stream>>>(a);
       ST_TRY(check_launch(h, "bfactor_kernel<tail>"));
+    }
+    if (h->use_tiles && h->n_tiles > 0) {
+      BTileArgs& ta = h->tile_args;
+      ta.gen = h->gen;
+      ta.ticket = h->d_tickets + 1;
+      h->tile_fn<<<h->tile_grid, (h->tile_rows_per + 1) * 32, h->tile_smem, h->stream>>>(ta);
+      ST_TRY(check_launch(h, "bfactor_tile_kernel"));
     }
     if (h->n_blocks > 0) {
       BBlockArgs bb;
@@ -758,6 +781,121 @@ b200lu_status classic_batch(H* h, const double* b, const double* x0, int use_pre
   return B200LU_OK;
 }
 
+// ---- tiled trailing part (tile.cuh / tile_plan.hpp)
+
+using TileFn = void (*)(BTileArgs);
+
+// Builds the tile plan for the (ascending) trailing rows and uploads it. Leaves h->use_tiles false, with
+// the reason in h->tile_note, when the pattern cannot be tiled.
+b200lu_status setup_tiles(H* h, const std::vector<int32_t>& tail_rows) {
+  const Schedule& S = h->sched;
+  cudaDeviceProp prop;
+  CU_TRY(h, cudaGetDeviceProperties(&prop, h->device));
+  const char* e = std::getenv("B200LU_TILE_ROWS");
+  const int R = e && std::atoi(e) == 16 ? 16 : 8;
+  // Shared memory of a tile: the ring, the rows, the control block. Default budget: what lets
+  // B200LU_TILE_CTAS (2 at R = 16, 3 at R = 8) CTAs share an SM; a pattern with a row that needs more gets
+  // the whole SM for one CTA.
+  e = std::getenv("B200LU_TILE_CTAS");
+  const int ctas = std::max(1, e ? std::atoi(e) : (R == 16 ? 2 : 3));
+  const int64_t sm_bytes = static_cast<int64_t>(prop.sharedMemPerMultiprocessor);
+  const int64_t max_block = static_cast<int64_t>(prop.sharedMemPerBlockOptin);
+  const int64_t overhead = static_cast<int64_t>(kTileRingBytes) + kTileCtlBytes + 128;
+  int64_t max_row = 0;
+  for (int32_t i : tail_rows) max_row = std::max<int64_t>(max_row, S.row_ptr[i + 1] - S.row_ptr[i]);
+  const int64_t row_bytes = static_cast<int64_t>(kTileScen * sizeof(double));
+  int64_t budget = std::min(max_block, sm_bytes / ctas - 1024) - overhead;  // 1 KB per CTA is reserved by the driver
+  if (max_row * row_bytes > budget) budget = max_block - overhead;
+  if (budget < max_row * row_bytes) {
+    h->tile_note = "a trailing row of " + std::to_string(max_row) + " entries does not fit a tile";
+    return B200LU_OK;
+  }
+  if (static_cast<int64_t>(h->groups) * h->nnz_factors >= (int64_t{1} << 31) - 4096) {
+    h->tile_note = "groups x nnz(L+U) exceeds the tensor-map coordinate range";
+    return B200LU_OK;
+  }
+  TilePlan plan;
+  const std::string err = build_tile_plan(S, tail_rows, R, budget / row_bytes, plan);
+  if (!err.empty()) {
+    h->tile_note = err;
+    return B200LU_OK;
+  }
+  h->tile_rows_per = R;
+  h->n_tiles = static_cast<int32_t>(plan.tiles.size());
+  h->tile_units = h->padded / kTileScen;
+  h->tile_fetched_entries = plan.fetched_entries;
+  h->tile_args.rows_smem_bytes = static_cast<int32_t>(plan.rows_smem_entries * row_bytes);
+  h->tile_smem = static_cast<size_t>(h->tile_args.rows_smem_bytes + overhead);
+  ST_TRY(dev_upload(h, &h->d_tile_meta, plan.tiles));
+  ST_TRY(dev_upload(h, &h->d_tile_rows, plan.rows));
+  ST_TRY(dev_upload(h, &h->d_tile_ext, plan.ext));
+  ST_TRY(dev_upload(h, &h->d_tile_row_items, plan.row_items));
+  ST_TRY(dev_upload(h, &h->d_tile_dest, plan.tdest));
+  ST_TRY(dev_alloc(h, &h->d_tile_flags, static_cast<size_t>(h->n) * h->tile_units));
+  CU_TRY(h, cudaMemsetAsync(h->d_tile_flags, 0, static_cast<size_t>(h->n) * h->tile_units * sizeof(int32_t), h->stream));
+  h->use_tiles = true;
+  return B200LU_OK;
+}
+
+// Tensor maps, kernel attributes and grid of the tiled launch (after d_values / d_dest exist).
+b200lu_status finish_tiles(H* h, int sm_count) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qres;
+  CU_TRY(h, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
+  if (!fn || qres != cudaDriverEntryPointSuccess) {
+    h->last_error = "cuTensorMapEncodeTiled is not available from this driver";
+    return B200LU_CUDA_ERROR;
+  }
+  BTileArgs& ta = h->tile_args;
+  // values viewed as a 2-D tensor: [groups * nnz_factors] rows of 32 doubles; a box is 8 scenarios wide
+  const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(h->groups) * static_cast<cuuint64_t>(h->nnz_factors)};
+  const cuuint64_t strides[1] = {32 * sizeof(double)};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int i = 0; i < kTileMaps; ++i) {
+    const cuuint32_t box[2] = {kTileScen, static_cast<cuuint32_t>(kTileBoxStep * (i + 1))};
+    const CUresult r = reinterpret_cast<EncodeFn>(fn)(&ta.maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->d_values, dims, strides, box,
+                                                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      h->last_error = "cuTensorMapEncodeTiled failed with code " + std::to_string(static_cast<int>(r));
+      return B200LU_CUDA_ERROR;
+    }
+  }
+  ta.n_tiles = h->n_tiles;
+  ta.units = h->tile_units;
+  ta.gen = 0;
+  ta.tiles = h->d_tile_meta;
+  ta.rows = h->d_tile_rows;
+  ta.ext = h->d_tile_ext;
+  ta.row_items = h->d_tile_row_items;
+  ta.tdest = reinterpret_cast<const uint4*>(h->d_tile_dest);
+  ta.values = h->d_values;
+  ta.nnz_factors = h->nnz_factors;
+  ta.flags = h->d_tile_flags;
+  ta.pivot_floor = h->pivot_floor;
+  ta.failed = h->d_failed;
+  ta.ticket = h->d_tickets + 1;
+  h->tile_fn = h->tile_rows_per == 16 ? bfactor_tile_kernel<16> : bfactor_tile_kernel<8>;
+  // per function, process-wide: never lowered under a live handle (the largest request so far stays)
+  static size_t attr_set[2] = {0, 0};
+  size_t& cur = attr_set[h->tile_rows_per == 16];
+  if (h->tile_smem > cur) {
+    CU_TRY(h, cudaFuncSetAttribute(h->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->tile_smem)));
+    cur = h->tile_smem;
+  }
+  int occ = 0;
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->tile_fn, (h->tile_rows_per + 1) * 32, h->tile_smem));
+  if (occ < 1) {
+    h->last_error = "tiled factor kernel does not fit on an SM";
+    return B200LU_CUDA_ERROR;
+  }
+  h->tile_grid = sm_count * occ;
+  return B200LU_OK;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -843,10 +981,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     const int64_t tail_width = e ? std::atoll(e) : 1024;
     e = std::getenv("B200LU_BATCH_TAIL_MODE");
     const int tail_mode = e ? std::atoi(e) : 1;
-    const int64_t levels = static_cast<int64_t>(S.lower_width.size());
-    int64_t cut = levels;
-    for (int64_t l = levels - 1; l >= 1 && S.lower_width[l] < tail_width; --l) cut = l;
-    if (levels - cut < 16) cut = levels;  // not worth a second launch
+    const int64_t cut = trailing_cut_level(S, tail_width);
     std::vector<FactorMeta> meta;
     meta.reserve(n);
     std::vector<int32_t> tail_rows;
@@ -870,6 +1005,18 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       tail_rows.clear();
     }
     std::sort(tail_rows.begin(), tail_rows.end());
+    // B200LU_BATCH_TILES (default 1): the trailing part in CTA tiles resident in shared memory (tile.cuh).
+    // 0, or a pattern / batch the tiled kernel cannot take (a row larger than a tile, more than 2^31
+    // entries per tensor-map dimension): the row-blocked kernel below.
+    e = std::getenv("B200LU_BATCH_TILES");
+    if ((!e || std::atoi(e) != 0) && !tail_rows.empty() && tail_mode != 0) {
+      ST_TRY(setup_tiles(h, tail_rows));
+      if (h->use_tiles) {
+        h->n_block_rows = static_cast<int32_t>(tail_rows.size());
+        for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+        tail_rows.clear();
+      }
+    }
     std::vector<BlockMeta> blocks;
     std::vector<MergedPivot> merged;
     for (size_t b0 = 0; b0 < tail_rows.size(); b0 += kBlockRows) {
@@ -1038,6 +1185,7 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   // launch geometry: persistent grids sized to what is co-resident
   cudaDeviceProp prop;
   CU_TRY(h, cudaGetDeviceProperties(&prop, h->device));
+  if (h->use_tiles) ST_TRY(finish_tiles(h, prop.multiProcessorCount));
   {
     using Fn = void (*)(BFactorArgs);
     // variant = (min CTAs per SM -> register cap, loads in flight per warp); B200LU_BATCH_VARIANT for experiments
@@ -1121,7 +1269,7 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
                   h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
@@ -1355,7 +1503,7 @@ b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* ou
   out->unit_scenarios = h->unit;
   out->factor_rows = h->n_factor_rows + h->n_block_rows;
   out->blocked_rows = h->n_block_rows;
-  out->blocks = h->n_blocks;
+  out->blocks = h->use_tiles ? h->n_tiles : h->n_blocks;
   out->blocked_pairs = h->blocked_pairs;
   out->factor_grid = h->factor_grid;
   out->tri_grid = h->tri_grid;
@@ -1368,7 +1516,79 @@ b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* ou
   out->device_bytes = h->device_bytes;
   out->alloc_events = h->alloc_events;
   out->launches = static_cast<int64_t>(h->launches);
+  out->tiled = h->use_tiles ? 1 : 0;
+  out->tile_rows = h->use_tiles ? h->tile_rows_per : 0;
+  out->tile_smem_bytes = h->use_tiles ? static_cast<int64_t>(h->tile_smem) : 0;
+  out->tile_grid = h->use_tiles ? h->tile_grid : 0;
+  out->tile_fetched_entries = h->tile_fetched_entries;
   return B200LU_OK;
+}
+
+b200lu_status b200lu_tile_plan_emulate(const b200lu_symbolic_view* sym, int rows_per_tile, int64_t tile_entries,
+                                       int64_t tail_width, double pivot_floor, double* values, int64_t* failed_row,
+                                       b200lu_tile_plan_stats* stats, char* error_buf, int error_buf_len) {
+  auto fail = [&](const std::string& msg) {
+    if (error_buf && error_buf_len > 0) {
+      std::strncpy(error_buf, msg.c_str(), static_cast<size_t>(error_buf_len) - 1);
+      error_buf[error_buf_len - 1] = 0;
+    }
+    return B200LU_INVALID_ARGUMENT;
+  };
+  if (!sym || !values || rows_per_tile < 1 || tile_entries < 1) return fail("null or non-positive argument");
+  Schedule S;
+  ScheduleTuning tune;
+  tune.tail_min_levels = int64_t{1} << 40;
+  const std::string err = build_schedule(*sym, tune, S);
+  if (!err.empty()) return fail(err);
+  const int64_t cut = trailing_cut_level(S, tail_width);
+  std::vector<int32_t> tail_rows;
+  int64_t failed = -1;
+  auto note_pivot = [&](int32_t i) {
+    if (std::fabs(values[S.diag[i]]) <= pivot_floor && (failed < 0 || i < failed)) failed = i;
+  };
+  // head rows: plain up-looking elimination in dependency-level order (what the head launch does)
+  for (int32_t i : S.lower_order) {
+    if (S.diag[i] == S.row_ptr[i]) {
+      note_pivot(i);
+      continue;
+    }
+    if (S.lower_level[i] >= cut) {
+      tail_rows.push_back(i);
+      continue;
+    }
+    for (int32_t k = S.row_ptr[i]; k < S.diag[i]; ++k) {
+      const int32_t d = S.col[k], dd = S.diag[d];
+      const double alpha = values[k] / values[dd];
+      values[k] = alpha;
+      int32_t pos = k + 1;
+      for (int32_t t = dd + 1; t < S.row_ptr[d + 1]; ++t) {
+        while (S.col[pos] < S.col[t]) ++pos;
+        const double prod = alpha * values[t];
+        values[pos] = values[pos] - prod;
+      }
+    }
+    note_pivot(i);
+  }
+  std::sort(tail_rows.begin(), tail_rows.end());
+  TilePlan plan;
+  const std::string perr = build_tile_plan(S, tail_rows, rows_per_tile, tile_entries, plan);
+  if (!perr.empty()) return fail(perr);
+  const int64_t f2 = emulate_tile_plan(S, plan, pivot_floor, values);
+  if (f2 <= -2) return fail("plan error " + std::to_string(f2) + ": the tile plan is inconsistent");
+  if (f2 >= 0 && (failed < 0 || f2 < failed)) failed = f2;
+  if (failed_row) *failed_row = failed;
+  if (stats) {
+    stats->tiles = static_cast<int64_t>(plan.tiles.size());
+    stats->rows = static_cast<int64_t>(plan.rows.size());
+    stats->items = static_cast<int64_t>(plan.ext.size());
+    stats->fetched_entries = plan.fetched_entries;
+    stats->pairs = plan.pairs;
+    stats->largest_tile_entries = plan.rows_smem_entries;
+    int64_t consumed = 0;
+    for (const ExtItem& q : plan.ext) consumed += static_cast<int64_t>(q.cnt_flags & 0xffffu) * __builtin_popcount(q.users);
+    stats->consumed_entries = consumed;
+  }
+  return failed >= 0 ? B200LU_ZERO_PIVOT : B200LU_OK;
 }
 
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled) {

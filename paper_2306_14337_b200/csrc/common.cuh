@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace b200lu {
 
@@ -114,6 +115,8 @@ __device__ __forceinline__ double add_prod(double a, double b, double c) {
 template <typename Arg>
 inline cudaError_t launch_resident(void (*kernel)(Arg), int grid, int block, size_t smem, cudaStream_t stream, Arg arg) {
   void* params[] = {&arg};
+  static const bool plain = [] { const char* e = getenv("B200LU_COOP_LAUNCH"); return e && e[0] == '0'; }();
+  if (plain) return cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(block), params, smem, stream);
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(block), params, smem, stream);
 }
 

@@ -1,0 +1,311 @@
+// K2 batched, trailing part: CTA tiles of consecutive rows with the target rows RESIDENT IN SHARED
+// MEMORY and the pivot rows streamed once per tile by TMA (sm_100a).
+//
+// Why. eliminate (src/numeric.cpp:27-58) applies, for every strict-lower entry (i, d) of row i in
+// ascending d, a_ij <- a_ij - (a_id / u_dd) * u_dj over the upper entries of row d. In a scenario batch
+// the row-per-warp kernels (batch.cuh) sent every one of those updates to L2 as a reduction: 12 G
+// updates = 96 GB through the L2 atomic unit per refactorization at C2 x 256, the unit 70 % busy, and
+// every pivot row re-read from L2/DRAM once per consumer row (19 on average). Here
+//   * a unit of work is (tile of up to R index-consecutive rows) x (8 scenarios); every row of the
+//     tile lives in shared memory from its first update to its last, so an update is a plain ordered
+//     read-modify-write of shared memory — one owner warp per row, pivots in ascending order, the same
+//     two roundings as the reference: bit-exact by construction — and the row is read from and written
+//     to HBM exactly once;
+//   * the rows of a tile share most of their pivots (consecutive rows of the trailing part are
+//     ancestors of the same subtrees: measured reuse 5.3x at R = 8, 7.8x at R = 16 on the C2 pattern),
+//     so each pivot row is fetched ONCE per tile: a producer warp walks the ascending merge of the
+//     tile's pivot lists, waits for the pivot row's ready flag (ld.acquire), and issues one 2-D TMA
+//     copy (cp.async.bulk.tensor, box = 8 scenarios x up to 96 entries) into a ring of stages guarded
+//     by mbarriers; the consumer warps never touch global memory for a pivot row;
+//   * a pivot that is itself a row of the tile is read straight from its owner's shared-memory copy
+//     (hand-off through a shared-memory flag: the chain of consecutive rows advances at on-chip latency
+//     inside a tile and crosses L2 once per tile);
+//   * lanes = 8 entry lanes x 4 scenario pairs: every shared-memory access is 16 bytes (two scenarios of
+//     one entry), a pivot row of m entries costs m/8 dependent steps, and the destination offsets of 64
+//     entries arrive in one 16-byte load per lane from a table laid out for exactly this access.
+// Tiles are claimed with an atomic ticket in a topological order of the tile DAG, so a claimed tile only
+// ever waits for rows of tiles that are finished or resident.
+#pragma once
+
+#include <cuda.h>
+
+#include "batch.cuh"
+#include "tile_plan.hpp"
+
+namespace b200lu {
+
+constexpr int kTileCtlBytes = 1024;
+constexpr int kTileBlockDoubles = kTileBoxStep * kTileScen;  // one ring block: 16 entries x 8 scenarios = 1 KB
+constexpr size_t kTileRingBytes = static_cast<size_t>(kTileRingBlocks) * kTileBlockDoubles * sizeof(double) + 128;  // + over-read slack
+
+struct BTileArgs {
+  CUtensorMap maps[kTileMaps];  // values viewed as [groups * nnz_factors][32] doubles, box 8 x (16 * (i + 1))
+  int32_t n_tiles, units, gen;
+  int32_t rows_smem_bytes;
+  const TileMeta* tiles;
+  const TileRow* rows;
+  const ExtItem* ext;
+  const RowItem* row_items;
+  const uint4* tdest;           // tile destination table, 16-byte words (tile_plan.hpp)
+  double* values;
+  int64_t nnz_factors;
+  int32_t* flags;               // [n][units] generation per (row, 8-scenario unit)
+  double pivot_floor;
+  int32_t* failed;
+  unsigned long long* ticket;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t addr = smem_u32(bar);
+  while (!ok) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(addr), "r"(parity)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(smem_u32(smem_dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void st_release_s32(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__((R + 1) * 32)
+bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
+  static_assert(R <= kTileMaxRows, "users mask / control block");
+  // dynamic shared memory starts behind the 1 KB the system reserves per CTA: 128-byte aligned, which
+  // the TMA destinations need (checked once below)
+  extern __shared__ __align__(128) unsigned char tile_smem_raw[];
+  unsigned char* base = tile_smem_raw;
+  double* ring = reinterpret_cast<double*>(base);  // [block][16 entries][8 scenarios]
+  double* rowsm = reinterpret_cast<double*>(base + kTileRingBytes);
+  unsigned char* ctl = reinterpret_cast<unsigned char*>(rowsm) + a.rows_smem_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);                                // [slots] TMA arrival
+  int32_t* released = reinterpret_cast<int32_t*>(ctl + 128);                        // [slots] consumers done with the copy
+  volatile int32_t* slot_blk = reinterpret_cast<volatile int32_t*>(ctl + 192);      // [slots] first ring block of the copy
+  int32_t* p_expect = reinterpret_cast<int32_t*>(ctl + 256);                        // [slots] producer: consumers of the copy
+  int32_t* p_blocks = reinterpret_cast<int32_t*>(ctl + 320);                        // [slots] producer: ring blocks it holds
+  volatile int32_t* done = reinterpret_cast<volatile int32_t*>(ctl + 384);          // [R] row finished (intra-tile hand-off)
+  int32_t* uoff = reinterpret_cast<int32_t*>(ctl + 448);                            // [R] entry offset of each row's diagonal
+  volatile int32_t* issued = reinterpret_cast<volatile int32_t*>(ctl + 512);        // copies issued so far (monotone over tiles)
+  unsigned long long* s_ticket = reinterpret_cast<unsigned long long*>(ctl + 520);
+
+  const unsigned fullmask = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sp = lane & 3, e = lane >> 2;  // scenario pair (scenarios 2 sp, 2 sp + 1) and entry lane
+  if (threadIdx.x == 0) {
+    if (smem_u32(base) & 127u) __trap();
+    for (int i = 0; i < kTileSlots; ++i) {
+      mbar_init(full + i, 1);
+      released[i] = 0;
+    }
+    *issued = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  int32_t ext_base = 0;  // copies issued for the tiles this CTA has already processed
+  const unsigned long long total = static_cast<unsigned long long>(a.n_tiles) * a.units;
+  while (true) {
+    __syncthreads();  // the previous tile is finished: its shared memory may be reused
+    if (threadIdx.x == 0) *s_ticket = atomicAdd(a.ticket, 1ull);
+    if (threadIdx.x < R) done[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long t = *s_ticket;
+    if (t >= total) break;
+    const int32_t b = static_cast<int32_t>(t / a.units);
+    const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units);
+    const int4 tm = __ldg(reinterpret_cast<const int4*>(a.tiles + b));
+    const int32_t row_beg = tm.x, nrows = tm.y, ext_beg = tm.z, n_ext = tm.w;
+    // unit u = scenarios [8u, 8u + 8): group of 32 = u / 4, quarter = u % 4
+    const int64_t group_base = static_cast<int64_t>(u >> 2) * a.nnz_factors;
+    double* gq = a.values + group_base * 32 + (u & 3) * kTileScen;
+
+    if (warp == R) {
+      // ------------------------------------------------------------ producer warp
+      // Lanes fetch the records of 32 copies at a time and probe the ready flags of their pivot rows in
+      // parallel; lane 0 then issues the copies in order: ring space (the oldest copies are retired once
+      // all their consumers have released them), the flag if the probe found it unset, one TMA copy.
+      int32_t head = 0, used = 0, oldest = 0;  // lane 0: ring allocator state of this tile
+      for (int32_t b0 = 0; b0 < n_ext; b0 += 32) {
+        int4 my = make_int4(0, 0, 0, 0);
+        int32_t ready = 1;
+        if (b0 + lane < n_ext) {
+          my = __ldg(reinterpret_cast<const int4*>(a.ext + ext_beg + b0 + lane));
+          if ((static_cast<uint32_t>(my.w) >> 16) & kItemWait) {
+            ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my.y) * a.units + u) >= a.gen;
+          }
+        }
+        __syncwarp();
+        const int nq = min(32, n_ext - b0);
+        for (int q = 0; q < nq; ++q) {
+          const int32_t entry = __shfl_sync(fullmask, my.x, q);
+          const int32_t d = __shfl_sync(fullmask, my.y, q);
+          const uint32_t users = static_cast<uint32_t>(__shfl_sync(fullmask, my.z, q));
+          const uint32_t cf = static_cast<uint32_t>(__shfl_sync(fullmask, my.w, q));
+          const int32_t rdy = __shfl_sync(fullmask, ready, q);
+          if (lane == 0) {
+            const int32_t x = b0 + q, gx = ext_base + x;
+            const int slot = gx & (kTileSlots - 1);
+            const int nb = (static_cast<int>(cf & 0xffffu) + kTileBoxStep - 1) / kTileBoxStep;  // 1..kTileMaps blocks
+            const bool wrap = head + nb > kTileRingBlocks;  // a copy is contiguous: skip the blocks left at the end
+            const int waste = wrap ? kTileRingBlocks - head : 0;
+            while (x - oldest >= kTileSlots || used + nb + waste > kTileRingBlocks) {
+              const int os = (ext_base + oldest) & (kTileSlots - 1);
+              while (*reinterpret_cast<volatile int32_t*>(released + os) != p_expect[os]) __nanosleep(32);
+              used -= p_blocks[os];
+              ++oldest;
+            }
+            if (wrap) head = 0;
+            const int start = head;
+            head += nb;
+            used += nb + waste;
+            *reinterpret_cast<volatile int32_t*>(released + slot) = 0;
+            p_expect[slot] = __popc(users);
+            p_blocks[slot] = nb + waste;
+            slot_blk[slot] = start;
+            if (!rdy) {  // (a flag the probe found set was acquired by another lane; the __syncwarp below the
+              const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;  // probe orders it for this one)
+              unsigned ns = 32;
+              while (ld_acquire_s32(f) < a.gen) {
+                __nanosleep(ns);
+                ns = min(ns * 2, 256u);
+              }
+            }
+            // the pivot row was written through the generic proxy (by this or another SM) and is read by
+            // the async proxy: order the two behind the acquire
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(nb * kTileBlockDoubles * sizeof(double)));
+            tma_load_2d(ring + static_cast<size_t>(start) * kTileBlockDoubles, &a.maps[nb - 1], (u & 3) * kTileScen,
+                        static_cast<int32_t>(group_base + entry), full + slot);
+            __threadfence_block();
+            *issued = gx + 1;
+          }
+          __syncwarp();
+        }
+      }
+    } else if (warp < nrows) {
+      // ------------------------------------------------------------ consumer: one row of the tile
+      const int4 r0 = __ldg(reinterpret_cast<const int4*>(a.rows + row_beg + warp));
+      const int4 r1 = __ldg(reinterpret_cast<const int4*>(a.rows + row_beg + warp) + 1);
+      const int32_t i = r0.x, lo = r0.y, len = r0.z, nl = r0.w;
+      const int32_t ri_beg = r1.x, ri_cnt = r1.y;
+      double* myrow = rowsm + static_cast<size_t>(r1.z) * kTileScen;
+      double* myrow2 = myrow + 2 * sp;  // this lane's two scenarios of entry 0
+      double* grow = gq + static_cast<int64_t>(lo) * 32;
+      if (lane == 0) uoff[warp] = r1.z + nl;  // read by the other rows only behind done[warp]
+      // the row as the scatter pass left it: global -> shared, 16 bytes per lane, 8 entries per instruction
+      for (int32_t j = lane >> 2; j < len; j += 8) {
+        cp_async_16(myrow + static_cast<size_t>(j) * kTileScen + (lane & 3) * 2, grow + static_cast<int64_t>(j) * 32 + (lane & 3) * 2);
+      }
+      if (e == 0) *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(len) * kTileScen) = make_double2(0.0, 0.0);  // the spare entry
+      cp_async_commit_wait_all();
+      __syncwarp();
+
+      int32_t k = 0;  // pivots of this row applied so far
+      double2 alpha = make_double2(0.0, 0.0);
+      for (int32_t b0 = 0; b0 < ri_cnt; b0 += 32) {
+        int4 mine = make_int4(0, 0, 0, 0);
+        if (b0 + lane < ri_cnt) mine = __ldg(reinterpret_cast<const int4*>(a.row_items + ri_beg + b0 + lane));
+        const int nq = min(32, ri_cnt - b0);
+        for (int q = 0; q < nq; ++q) {
+          const uint32_t toff = static_cast<uint32_t>(__shfl_sync(fullmask, mine.x, q));
+          const int32_t srcid = __shfl_sync(fullmask, mine.y, q);
+          int32_t cnt = __shfl_sync(fullmask, mine.z, q);
+          const uint32_t fl = static_cast<uint32_t>(__shfl_sync(fullmask, mine.w, q));
+          // the destinations of the first four iterations (64 entries), requested before the waits below
+          const uint4* __restrict__ tw = a.tdest + static_cast<size_t>(toff) * kTileEntryLanes + e;
+          uint4 wd = __ldg(tw);
+          const bool internal = (fl & kItemInternal) != 0;
+          const double* src;
+          int slot = 0;
+          if (internal) {
+            while (done[srcid] == 0) __nanosleep(32);
+            __threadfence_block();
+            src = rowsm + static_cast<size_t>(uoff[srcid]) * kTileScen;
+          } else {
+            const int32_t gx = ext_base + srcid;
+            slot = gx & (kTileSlots - 1);
+            while (*issued <= gx) __nanosleep(64);
+            mbar_wait(full + slot, static_cast<uint32_t>(gx / kTileSlots) & 1u);
+            src = ring + static_cast<size_t>(slot_blk[slot]) * kTileBlockDoubles;
+          }
+          const double* sl = src + e * kTileScen + 2 * sp;
+          if (fl & kItemFirst) {
+            const double2 aik = *reinterpret_cast<const double2*>(myrow2 + static_cast<size_t>(k) * kTileScen);
+            const double2 udd = *reinterpret_cast<const double2*>(src + 2 * sp);
+            alpha.x = aik.x / udd.x;  // src/numeric.cpp:40
+            alpha.y = aik.y / udd.y;
+            sl += kTileScen;  // the diagonal is entry 0 of a first chunk
+            --cnt;
+          }
+          const int32_t iters = (cnt + kTileIter - 1) / kTileIter;
+          for (int32_t g0 = 0; g0 < iters; g0 += kTileGroup) {
+            const uint4 w = wd;
+            if (g0 + kTileGroup < iters) wd = __ldg(tw + static_cast<size_t>(g0 / kTileGroup + 1) * kTileEntryLanes);
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int i4 = 0; i4 < kTileGroup; ++i4) {
+              if (g0 + i4 < iters) {  // warp-uniform
+                const double* up = sl + static_cast<size_t>(g0 + i4) * kTileIter * kTileScen;
+                const double2 u0 = *reinterpret_cast<const double2*>(up);
+                const double2 u1 = *reinterpret_cast<const double2*>(up + kTileEntryLanes * kTileScen);
+                double2* p0 = reinterpret_cast<double2*>(myrow2 + (ww[i4] & 0xffffu) * kTileScen);
+                double2* p1 = reinterpret_cast<double2*>(myrow2 + (ww[i4] >> 16) * kTileScen);
+                double2 a0 = *p0, a1 = *p1;
+                a0.x = __dsub_rn(a0.x, __dmul_rn(alpha.x, u0.x));  // src/numeric.cpp:44
+                a0.y = __dsub_rn(a0.y, __dmul_rn(alpha.y, u0.y));
+                a1.x = __dsub_rn(a1.x, __dmul_rn(alpha.x, u1.x));
+                a1.y = __dsub_rn(a1.y, __dmul_rn(alpha.y, u1.y));
+                *p0 = a0;
+                *p1 = a1;
+              }
+            }
+          }
+          __syncwarp();  // every lane's updates are in shared memory before the next pivot reads them
+          if (!internal && lane == 0) atomicAdd(released + slot, 1);
+          if (fl & kItemLast) {
+            if (e == 0) *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(k) * kTileScen) = alpha;  // l_id, src/numeric.cpp:41
+            ++k;
+          }
+        }
+      }
+      // ---- the row is final. Order: (1) intra-tile hand-off, (2) pivot check, (3) diagonal + upper part to
+      // global memory and the ready flag (what other tiles wait for), (4) the lower part.
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) done[warp] = 1;
+      if (e == 0) {  // src/numeric.cpp:48; the row is published anyway
+        const double2 dg = *reinterpret_cast<const double2*>(myrow2 + static_cast<size_t>(nl) * kTileScen);
+        if (fabs(dg.x) <= a.pivot_floor) atomicMin(a.failed + u * kTileScen + 2 * sp, i);
+        if (fabs(dg.y) <= a.pivot_floor) atomicMin(a.failed + u * kTileScen + 2 * sp + 1, i);
+      }
+      for (int32_t j = nl + (lane >> 2); j < len; j += 8) {
+        const double2 v = *reinterpret_cast<const double2*>(myrow + static_cast<size_t>(j) * kTileScen + (lane & 3) * 2);
+        __stcg(reinterpret_cast<double2*>(grow + static_cast<int64_t>(j) * 32 + (lane & 3) * 2), v);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release_s32(a.flags + static_cast<int64_t>(i) * a.units + u, a.gen);
+      }
+      for (int32_t j = lane >> 2; j < nl; j += 8) {
+        const double2 v = *reinterpret_cast<const double2*>(myrow + static_cast<size_t>(j) * kTileScen + (lane & 3) * 2);
+        __stcg(reinterpret_cast<double2*>(grow + static_cast<int64_t>(j) * 32 + (lane & 3) * 2), v);
+      }
+    }
+    ext_base += n_ext;
+  }
+}
+
+}  // namespace b200lu

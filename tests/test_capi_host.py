@@ -114,3 +114,65 @@ def test_schedule_probe_rejects_broken_patterns():
         v.col_indices = bad_cols.ctypes.data
         st = _capi.lib().b200lu_schedule_probe(C.byref(v), None, None, None, None, err, 256)
         assert st == _capi.INVALID_ARGUMENT
+
+
+def _emulate(fx, k, rows_per_tile, tile_entries, tail_width, pivot_floor=1e-30, values=None):
+    vals = fx.oracle.scatter_values(fx.values[k] if values is None else values)
+    failed = C.c_int64(-1)
+    stats = _capi.TilePlanStats()
+    err = C.create_string_buffer(256)
+    st = _capi.lib().b200lu_tile_plan_emulate(C.byref(_view(fx.sym)), rows_per_tile, tile_entries, tail_width,
+                                              pivot_floor, vals.ctypes.data, C.byref(failed), C.byref(stats), err, 256)
+    return st, vals, int(failed.value), stats, err.value.decode()
+
+
+@pytest.mark.parametrize("name", ["kkt_small", "kkt_small_mc64", "random_sparse_120_plain", "random_sparse_60"])
+@pytest.mark.parametrize("rows_per_tile,tile_entries", [(8, 4096), (16, 4096), (3, 150), (1, 400)])
+def test_tile_plan_reproduces_the_oracle_bitwise(name, rows_per_tile, tile_entries):
+    """The plan of the tiled batched refactorization (csrc/tile_plan.hpp: tiling, ascending pivot merge,
+    chunking of long pivot rows, destination offsets, topological claim order), executed on the host for
+    one system, gives the oracle's L/U bit for bit (eliminate, src/numeric.cpp:27-58). tail_width = a huge
+    number puts every level but the first into the tiled part."""
+    fx = golden_fixture(name)
+    max_row = int(np.diff(fx.sym.row_offsets).max())
+    tile_entries = max(tile_entries, max_row)
+    for k in range(len(fx.values)):
+        st, vals, failed, stats, err = _emulate(fx, k, rows_per_tile, tile_entries, 1 << 40)
+        assert st == _capi.OK, err
+        ref, ref_failed = fx.oracle.factorize(fx.values[k])
+        assert ref_failed == -1 and failed == -1
+        assert np.array_equal(vals, ref)
+        assert stats.rows > 0 and stats.tiles >= -(-stats.rows // rows_per_tile)
+        assert stats.fetched_entries <= stats.consumed_entries
+        assert stats.largest_tile_entries <= tile_entries
+
+
+def test_tile_plan_shares_pivot_rows_and_reports_zero_pivots():
+    fx = golden_fixture("kkt_small")
+    st, vals, failed, stats, err = _emulate(fx, 0, 8, 1 << 20, 1 << 40)
+    assert st == _capi.OK, err
+    assert stats.consumed_entries > 1.5 * stats.fetched_entries  # consecutive rows share their pivot rows
+    # a row that is too long for a tile is refused, not mangled
+    st, _, _, _, err = _emulate(fx, 0, 8, 4, 1 << 40)
+    assert st == _capi.INVALID_ARGUMENT and "exceeds" in err
+    # zero pivot: the lowest failing row, as eliminate reports it (src/numeric.cpp:48-55)
+    v = fx.values[0].copy()
+    ref, ref_failed = fx.oracle.factorize(v, pivot_floor=1e300)
+    st, vals, failed, _, _ = _emulate(fx, 0, 8, 1 << 20, 1 << 40, pivot_floor=1e300)
+    assert st == _capi.ZERO_PIVOT and failed == ref_failed
+    assert np.array_equal(vals, ref)
+
+
+def test_tile_plan_chunks_long_pivot_rows():
+    """Pivot rows longer than a TMA stage (96 entries) are cut into chunks: a dense 150 x 150 matrix has
+    upper parts of up to 149 entries."""
+    from tests.fixtures import dense_fixture, have_reference
+    if not have_reference():
+        pytest.skip("oracle/_ref/librlu_ref.so not built")
+    rng = np.random.default_rng(7)
+    M = rng.uniform(-1.0, 1.0, (150, 150)) + 150.0 * np.eye(150)
+    fx = dense_fixture(M)
+    st, vals, failed, stats, err = _emulate(fx, 0, 8, 4096, 1 << 40)
+    assert st == _capi.OK, err
+    assert stats.items > stats.rows  # chunked externals
+    assert np.array_equal(vals, fx.oracle.factorize(fx.values[0])[0])
