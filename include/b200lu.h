@@ -324,6 +324,26 @@ b200lu_status b200lu_batch_kkt_bind(b200lu_batch* h, int64_t n_primal, const dou
                                     const int64_t* diag_source_pos);
 b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on_device, double delta_p,
                                       double delta_d);
+/* Staged (pipelined) submission for a SEQUENCE of batches, the device-side shape of cli::solve_sequence's
+ * loop (src/cli.cpp:80-135): while batch k is factorized and solved, the inputs of batch k + 1 cross the bus
+ * on a dedicated copy stream into the staging buffer that is not in use, and the solutions of batch k leave on
+ * a third stream. Host buffers should be page-locked (cudaHostRegister / pinned allocation) for the copies
+ * to overlap. Typical loop:
+ *     stage_inputs(v[0], b[0]);
+ *     for k: refactorize_staged(); if (k + 1 < K) stage_inputs(v[k+1], b[k+1]); solve_refine_staged(.., x[k], ..);
+ *     staged_wait();                  // x[k] may be read only after staged_wait (or after the next-but-one call)
+ * stage_inputs: [batch][nnz_source] values and/or [batch][n] right-hand sides (either may be NULL to keep the
+ * previous one); returns at once. refactorize_staged = reset_values + factorize_scattered on the staged values
+ * (src/numeric.cpp:70-79). solve_refine_staged = solve_system (src/trisolve.cpp:90-119) on the staged
+ * right-hand sides, then fgmres_refine (src/refine.cpp:39-142) from that solution when `refine` != 0; the result
+ * is copied to host_x_out asynchronously. The second staging set (one more copy of the values, right-hand
+ * sides and solutions on the device) is allocated by the first stage_inputs call. */
+b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_values, const double* host_rhs);
+b200lu_status b200lu_batch_refactorize_staged(b200lu_batch* h, int64_t* failed_rows);
+b200lu_status b200lu_batch_solve_refine_staged(b200lu_batch* h, int refine, const b200lu_refine_config* cfg,
+                                               double* host_x_out, b200lu_refine_outcome* outcomes,
+                                               int64_t* failed_rows);
+b200lu_status b200lu_batch_staged_wait(b200lu_batch* h);
 b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out);
 
 /* Diagnostics — HOST ONLY, needs no device; not on any product path. Builds the tile plan the batched

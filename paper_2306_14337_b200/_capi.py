@@ -109,6 +109,10 @@ EXPORTS = {
     "b200lu_batch_relative_residual": (i32, [vp, vp, vp, i32, vp]),
     "b200lu_batch_refine_fgmres": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
     "b200lu_batch_refine_classic": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig), vp]),
+    "b200lu_batch_stage_inputs": (i32, [vp, vp, vp]),
+    "b200lu_batch_refactorize_staged": (i32, [vp, vp]),
+    "b200lu_batch_solve_refine_staged": (i32, [vp, i32, C.POINTER(RefineConfig), vp, vp, vp]),
+    "b200lu_batch_staged_wait": (i32, [vp]),
     "b200lu_batch_get_info": (i32, [vp, C.POINTER(BatchInfo)]),
     "b200lu_tile_plan_emulate": (i32, [C.POINTER(SymbolicView), i32, i64, i64, dbl, vp, C.POINTER(i64),
                                        C.POINTER(TilePlanStats), C.c_char_p, i32]),

@@ -84,7 +84,7 @@ struct b200lu_batch {
   RowItem* d_tile_row_items = nullptr;
   uint16_t* d_tile_dest = nullptr;
   int32_t* d_tile_flags = nullptr;  // [n][tile_units]
-  int32_t n_tiles = 0, tile_units = 0, tile_rows_per = 8;
+  int32_t n_tiles = 0, tile_units = 0, tile_rows_per = 8, tile_ring_blocks = 32, tile_ctas = 2;
   int64_t tile_fetched_entries = 0;
   void (*tile_fn)(BTileArgs) = nullptr;
   int tile_grid = 0;
@@ -120,6 +120,15 @@ struct b200lu_batch {
   int chain_warps = 8, chain_buf = kTriBufferedChain;
   int32_t upper_chain_rows = 0;  // leading rows of the U level order handled by the chain launch
   size_t factor_smem = 0;
+
+  // staged (pipelined) submission: the next system's inputs are copied H2D on their own stream while the
+  // current one is processed, results leave on a third stream (b200lu_batch_stage_inputs & co.)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_vals_used[2] = {nullptr, nullptr}, ev_rhs_used[2] = {nullptr, nullptr},
+              ev_x[2] = {nullptr, nullptr}, ev_x_out[2] = {nullptr, nullptr};
+  double *d_stage_vals[2] = {nullptr, nullptr}, *d_stage_rhs[2] = {nullptr, nullptr}, *d_stage_x[2] = {nullptr, nullptr};
+  int stage_fill = 0, stage_cur = -1;   // buffer the next stage_inputs fills; buffer holding the staged inputs
+  bool staged_vals = false, staged_rhs = false, staged_ready = false;
 
   int64_t alloc_events = 0, device_bytes = 0;
   uint64_t launches = 0;
@@ -791,18 +800,23 @@ b200lu_status setup_tiles(H* h, const std::vector<int32_t>& tail_rows) {
   const Schedule& S = h->sched;
   cudaDeviceProp prop;
   CU_TRY(h, cudaGetDeviceProperties(&prop, h->device));
+  // B200LU_TILE_ROWS: rows (consumer warps) per tile, 8 (default) or 16; B200LU_TILE_CTAS: CTAs that share an
+  // SM, 2 (default) or 3 (R = 8 only; the ring shrinks to 16 KB so that a 57 KB row still fits) — together
+  // they fix the shared-memory budget of a tile. A pattern with a row that needs more gets the whole SM
+  // for one CTA.
   const char* e = std::getenv("B200LU_TILE_ROWS");
   const int R = e && std::atoi(e) == 16 ? 16 : 8;
-  // Shared memory of a tile: the ring, the rows, the control block. Default budget: what lets
-  // B200LU_TILE_CTAS (2 at R = 16, 3 at R = 8) CTAs share an SM; a pattern with a row that needs more gets
-  // the whole SM for one CTA.
   e = std::getenv("B200LU_TILE_CTAS");
-  const int ctas = std::max(1, e ? std::atoi(e) : (R == 16 ? 2 : 3));
+  int ctas = std::max(1, e ? std::atoi(e) : 2);
+  if (R == 16) ctas = std::min(ctas, 2);
+  ctas = std::min(ctas, 3);
+  h->tile_ring_blocks = ctas == 3 ? 16 : 32;
+  h->tile_ctas = ctas;
   const int64_t sm_bytes = static_cast<int64_t>(prop.sharedMemPerMultiprocessor);
   const int64_t max_block = static_cast<int64_t>(prop.sharedMemPerBlockOptin);
-  const int64_t overhead = static_cast<int64_t>(kTileRingBytes) + kTileCtlBytes + 128;
+  const int64_t overhead = static_cast<int64_t>(tile_ring_bytes(h->tile_ring_blocks)) + kTileCtlBytes + 128;
   int64_t max_row = 0;
-  for (int32_t i : tail_rows) max_row = std::max<int64_t>(max_row, S.row_ptr[i + 1] - S.row_ptr[i]);
+  for (int32_t i : tail_rows) max_row = std::max<int64_t>(max_row, S.row_ptr[i + 1] - S.row_ptr[i] + kTileSpare);  // + the spare entries
   const int64_t row_bytes = static_cast<int64_t>(kTileScen * sizeof(double));
   int64_t budget = std::min(max_block, sm_bytes / ctas - 1024) - overhead;  // 1 KB per CTA is reserved by the driver
   if (max_row * row_bytes > budget) budget = max_block - overhead;
@@ -815,7 +829,7 @@ b200lu_status setup_tiles(H* h, const std::vector<int32_t>& tail_rows) {
     return B200LU_OK;
   }
   TilePlan plan;
-  const std::string err = build_tile_plan(S, tail_rows, R, budget / row_bytes, plan);
+  const std::string err = build_tile_plan(S, tail_rows, R, budget / row_bytes, plan, h->tile_ring_blocks);
   if (!err.empty()) {
     h->tile_note = err;
     return B200LU_OK;
@@ -878,10 +892,11 @@ b200lu_status finish_tiles(H* h, int sm_count) {
   ta.pivot_floor = h->pivot_floor;
   ta.failed = h->d_failed;
   ta.ticket = h->d_tickets + 1;
-  h->tile_fn = h->tile_rows_per == 16 ? bfactor_tile_kernel<16> : bfactor_tile_kernel<8>;
+  const int variant = h->tile_rows_per == 16 ? 1 : h->tile_ctas == 3 ? 2 : 0;
+  h->tile_fn = variant == 1 ? bfactor_tile_kernel<16, 32, 2> : variant == 2 ? bfactor_tile_kernel<8, 16, 3> : bfactor_tile_kernel<8, 32, 2>;
   // per function, process-wide: never lowered under a live handle (the largest request so far stays)
-  static size_t attr_set[2] = {0, 0};
-  size_t& cur = attr_set[h->tile_rows_per == 16];
+  static size_t attr_set[3] = {0, 0, 0};
+  size_t& cur = attr_set[variant];
   if (h->tile_smem > cur) {
     CU_TRY(h, cudaFuncSetAttribute(h->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->tile_smem)));
     cur = h->tile_smem;
@@ -1005,11 +1020,22 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       tail_rows.clear();
     }
     std::sort(tail_rows.begin(), tail_rows.end());
-    // B200LU_BATCH_TILES (default 1): the trailing part in CTA tiles resident in shared memory (tile.cuh).
-    // 0, or a pattern / batch the tiled kernel cannot take (a row larger than a tile, more than 2^31
-    // entries per tensor-map dimension): the row-blocked kernel below.
+    // The trailing part runs in one of two kernels:
+    //   * bfactor_tile_kernel (tile.cuh): CTA tiles of 8 rows x 8 scenarios resident in shared memory, pivot
+    //     rows staged once per tile by TMA, plain ordered read-modify-write updates. 3x less DRAM traffic and
+    //     no L2 reductions, and a dependency hand-off of ~1 us per level instead of ~8 us: the faster kernel
+    //     while the batch is LATENCY-bound. Measured, factor phase at C2: 32 scenarios 4.9 ms against 8.2 ms,
+    //     64: 8.1 against 9.7, 128: 14.9 against 14.1, 256: 27.6 against 24.4 (its per-(row, pivot) costs are
+    //     paid per 8 scenarios, the row-blocked kernel's per 32).
+    //   * bfactor_block_kernel (batch.cuh): 2-row blocks x 32 scenarios, updates as L2 reductions: the faster
+    //     one once the batch is THROUGHPUT-bound.
+    // B200LU_BATCH_TILES = 1 / 0 forces one of them; default: tiles up to 96 scenarios per handle (an 8-GPU
+    // shard of the 256-scenario batch is 32). A pattern / batch the tiled kernel cannot take (a row larger than
+    // a tile, a pivot row longer than a staging copy, more than 2^31 entries per tensor-map dimension) keeps
+    // the row-blocked kernel.
     e = std::getenv("B200LU_BATCH_TILES");
-    if ((!e || std::atoi(e) != 0) && !tail_rows.empty() && tail_mode != 0) {
+    const bool want_tiles = e ? std::atoi(e) != 0 : h->padded <= 96;
+    if (want_tiles && !tail_rows.empty() && tail_mode != 0) {
       ST_TRY(setup_tiles(h, tail_rows));
       if (h->use_tiles) {
         h->n_block_rows = static_cast<int32_t>(tail_rows.size());
@@ -1279,6 +1305,18 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   }
   for (cudaEvent_t e : h->ev_start) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_stop) cudaEventDestroy(e);
+  if (h->copy_in) cudaStreamSynchronize(h->copy_in);
+  if (h->copy_out) cudaStreamSynchronize(h->copy_out);
+  for (int i = 0; i < 2; ++i) {
+    for (cudaEvent_t e : {h->ev_in[i], h->ev_vals_used[i], h->ev_rhs_used[i], h->ev_x[i], h->ev_x_out[i]}) {
+      if (e) cudaEventDestroy(e);
+    }
+    for (double* q : {h->d_stage_vals[i], h->d_stage_rhs[i], h->d_stage_x[i]}) {
+      if (q && q != h->d_stage_a && q != h->d_stage_in && q != h->d_stage_out) cudaFree(q);
+    }
+  }
+  if (h->copy_in) cudaStreamDestroy(h->copy_in);
+  if (h->copy_out) cudaStreamDestroy(h->copy_out);
   if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->h_up) cudaFreeHost(h->h_up);
   if (h->h_failed) cudaFreeHost(h->h_failed);
@@ -1494,6 +1532,132 @@ b200lu_status b200lu_batch_refine_classic(b200lu_batch* h, const double* b, cons
                                           int use_preconditioner, const b200lu_refine_config* cfg,
                                           b200lu_refine_outcome* outcomes) {
   return batch_refine_common(h, b, x0, x_out, on_device, use_preconditioner, cfg, outcomes, false);
+}
+
+// ---- staged (pipelined) submission -------------------------------------------------------------------
+//
+// cli::solve_sequence (src/cli.cpp:80-135) hands the solver one system after the other; on a device the
+// inputs of system k + 1 can cross the bus while system k is factorized and solved. stage_inputs copies
+// on a dedicated stream into the buffer that is NOT in use (two of each), the *_staged calls make the
+// compute stream wait for that copy only, and the solution leaves on a third stream.
+
+static b200lu_status stage_setup(b200lu_batch* h) {
+  if (h->staged_ready) return B200LU_OK;
+  CU_TRY(h, cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+  CU_TRY(h, cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    for (cudaEvent_t* e : {&h->ev_in[i], &h->ev_vals_used[i], &h->ev_rhs_used[i], &h->ev_x[i], &h->ev_x_out[i]}) {
+      CU_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+  }
+  // buffer 0 is the handle's own staging set, buffer 1 is allocated on first use of the staged calls
+  h->d_stage_vals[0] = h->d_stage_a;
+  h->d_stage_rhs[0] = h->d_stage_in;
+  h->d_stage_x[0] = h->d_stage_out;
+  ST_TRY(dev_alloc(h, &h->d_stage_vals[1], static_cast<size_t>(h->nnz_source) * h->batch));
+  ST_TRY(dev_alloc(h, &h->d_stage_rhs[1], static_cast<size_t>(h->n) * h->batch));
+  ST_TRY(dev_alloc(h, &h->d_stage_x[1], static_cast<size_t>(h->n) * h->batch));
+  h->staged_ready = true;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_values, const double* host_rhs) {
+  if (!h || (!host_values && !host_rhs)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  ST_TRY(stage_setup(h));
+  const int buf = h->stage_fill;
+  // the buffer's previous contents must have been consumed by the compute stream
+  CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_vals_used[buf], 0));
+  CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_rhs_used[buf], 0));
+  if (host_values && h->nnz_source) {
+    CU_TRY(h, cudaMemcpyAsync(h->d_stage_vals[buf], host_values, static_cast<size_t>(h->nnz_source) * h->batch * sizeof(double),
+                              cudaMemcpyHostToDevice, h->copy_in));
+  }
+  if (host_rhs && h->n) {
+    CU_TRY(h, cudaMemcpyAsync(h->d_stage_rhs[buf], host_rhs, static_cast<size_t>(h->n) * h->batch * sizeof(double),
+                              cudaMemcpyHostToDevice, h->copy_in));
+  }
+  CU_TRY(h, cudaEventRecord(h->ev_in[buf], h->copy_in));
+  h->staged_vals = host_values != nullptr;
+  h->staged_rhs = host_rhs != nullptr;
+  h->stage_cur = buf;
+  h->stage_fill = buf ^ 1;
+  return B200LU_OK;
+}
+
+b200lu_status b200lu_batch_refactorize_staged(b200lu_batch* h, int64_t* failed_rows) {
+  if (!h) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->stage_cur < 0 || !h->staged_vals) {
+    h->last_error = "refactorize_staged: no staged values (call b200lu_batch_stage_inputs first)";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  const int buf = h->stage_cur;
+  CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[buf], 0));
+  std::fill(h->valid.begin(), h->valid.end(), 0);
+  h->have_values = true;
+  {
+    PhaseScope ps(h, B200LU_PHASE_SCATTER);
+    if (h->nnz_source) {
+      dim3 grid(static_cast<unsigned>((h->nnz_source + 31) / 32), static_cast<unsigned>(h->groups));
+      interleave_kernel<<<grid, 256, 0, h->stream>>>(h->nnz_source, h->batch, h->d_stage_vals[buf], h->d_a_int);
+      ST_TRY(check_launch(h, "interleave_kernel"));
+    }
+  }
+  CU_TRY(h, cudaEventRecord(h->ev_vals_used[buf], h->stream));
+  h->staged_vals = false;
+  ST_TRY(launch_scatter(h));
+  return launch_factor(h, failed_rows);
+}
+
+b200lu_status b200lu_batch_solve_refine_staged(b200lu_batch* h, int refine, const b200lu_refine_config* cfg_in,
+                                               double* host_x_out, b200lu_refine_outcome* outcomes, int64_t* failed_rows) {
+  for (int32_t s = 0; h && failed_rows && s < h->batch; ++s) failed_rows[s] = -1;
+  if (!h || (!host_x_out && h->n) || (refine && !outcomes)) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->stage_cur < 0 || !h->staged_rhs) {
+    h->last_error = "solve_refine_staged: no staged right-hand sides (call b200lu_batch_stage_inputs first)";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  ST_TRY(any_valid(h, "solve_system"));
+  if (h->n == 0) return B200LU_OK;
+  b200lu_refine_config cfg{20, 1e-14};
+  if (cfg_in) cfg = *cfg_in;
+  if (refine && cfg.max_iterations > h->refine_capacity) {
+    h->last_error = "max_iterations exceeds the handle's refine_capacity";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  const int buf = h->stage_cur;
+  CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[buf], 0));
+  ST_TRY(to_interleaved(h, h->n, h->d_stage_rhs[buf], h->d_b));
+  CU_TRY(h, cudaEventRecord(h->ev_rhs_used[buf], h->stream));
+  h->staged_rhs = false;
+  ST_TRY(solve_int(h, h->d_b, h->d_x));
+  b200lu_status fail = collect_upper_failure(h, failed_rows);
+  const double* result = h->d_x;
+  if (refine) {
+    ST_TRY(copy_dd(h, h->d_x0, h->d_x));
+    ST_TRY(fgmres_batch(h, h->d_b, h->d_x0, 1, cfg, outcomes));
+    result = h->d_best;
+  }
+  // the staging buffer's previous solution must have left the device before it is overwritten
+  CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_x_out[buf], 0));
+  ST_TRY(from_interleaved(h, h->n, result, h->d_stage_x[buf]));
+  CU_TRY(h, cudaEventRecord(h->ev_x[buf], h->stream));
+  CU_TRY(h, cudaStreamWaitEvent(h->copy_out, h->ev_x[buf], 0));
+  CU_TRY(h, cudaMemcpyAsync(host_x_out, h->d_stage_x[buf], static_cast<size_t>(h->n) * h->batch * sizeof(double),
+                            cudaMemcpyDeviceToHost, h->copy_out));
+  CU_TRY(h, cudaEventRecord(h->ev_x_out[buf], h->copy_out));
+  return fail;
+}
+
+b200lu_status b200lu_batch_staged_wait(b200lu_batch* h) {
+  if (!h) return B200LU_INVALID_ARGUMENT;
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (h->copy_in) CU_TRY(h, cudaStreamSynchronize(h->copy_in));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  if (h->copy_out) CU_TRY(h, cudaStreamSynchronize(h->copy_out));
+  return B200LU_OK;
 }
 
 b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* out) {

@@ -32,11 +32,18 @@
 #include "batch.cuh"
 #include "tile_plan.hpp"
 
+// Sleep (ns) between polls of the shared-memory progress words; 0 = plain spin.
+#ifndef B200LU_TILE_SPIN_NS
+#define B200LU_TILE_SPIN_NS 32
+#endif
+
 namespace b200lu {
 
-constexpr int kTileCtlBytes = 1024;
+constexpr int kTileCtlBytes = 1280;
 constexpr int kTileBlockDoubles = kTileBoxStep * kTileScen;  // one ring block: 16 entries x 8 scenarios = 1 KB
-constexpr size_t kTileRingBytes = static_cast<size_t>(kTileRingBlocks) * kTileBlockDoubles * sizeof(double) + 128;  // + over-read slack
+__host__ __device__ constexpr size_t tile_ring_bytes(int ring_blocks) {  // + over-read slack
+  return static_cast<size_t>(ring_blocks) * kTileBlockDoubles * sizeof(double) + 128;
+}
 
 struct BTileArgs {
   CUtensorMap maps[kTileMaps];  // values viewed as [groups * nnz_factors][32] doubles, box 8 x (16 * (i + 1))
@@ -77,12 +84,34 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
                ::"r"(smem_u32(smem_dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ int32_t ld_flag_relaxed(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// 16-byte shared-memory accesses through 32-bit shared addresses: the hot loops keep every address in one
+// register and never pay a generic->shared conversion (the compiler rematerialised one per access)
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ int32_t lds32_volatile(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_s32(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int R>
-__global__ void __launch_bounds__((R + 1) * 32)
+// R consumer warps (= rows of a tile) + 1 producer warp; RB ring blocks of 1 KB; MINB CTAs per SM the register
+// allocation must allow.
+template <int R, int RB, int MINB>
+__global__ void __launch_bounds__((R + 1) * 32, MINB)
 bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
   static_assert(R <= kTileMaxRows, "users mask / control block");
   // dynamic shared memory starts behind the 1 KB the system reserves per CTA: 128-byte aligned, which
@@ -90,17 +119,18 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
   extern __shared__ __align__(128) unsigned char tile_smem_raw[];
   unsigned char* base = tile_smem_raw;
   double* ring = reinterpret_cast<double*>(base);  // [block][16 entries][8 scenarios]
-  double* rowsm = reinterpret_cast<double*>(base + kTileRingBytes);
+  double* rowsm = reinterpret_cast<double*>(base + tile_ring_bytes(RB));
   unsigned char* ctl = reinterpret_cast<unsigned char*>(rowsm) + a.rows_smem_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl);                                // [slots] TMA arrival
   int32_t* released = reinterpret_cast<int32_t*>(ctl + 128);                        // [slots] consumers done with the copy
-  volatile int32_t* slot_blk = reinterpret_cast<volatile int32_t*>(ctl + 192);      // [slots] first ring block of the copy
   int32_t* p_expect = reinterpret_cast<int32_t*>(ctl + 256);                        // [slots] producer: consumers of the copy
   int32_t* p_blocks = reinterpret_cast<int32_t*>(ctl + 320);                        // [slots] producer: ring blocks it holds
   volatile int32_t* done = reinterpret_cast<volatile int32_t*>(ctl + 384);          // [R] row finished (intra-tile hand-off)
   int32_t* uoff = reinterpret_cast<int32_t*>(ctl + 448);                            // [R] entry offset of each row's diagonal
   volatile int32_t* issued = reinterpret_cast<volatile int32_t*>(ctl + 512);        // copies issued so far (monotone over tiles)
   unsigned long long* s_ticket = reinterpret_cast<unsigned long long*>(ctl + 520);
+  int4* p_items = reinterpret_cast<int4*>(ctl + 528);                               // [32] producer: records of the current batch
+  int32_t* p_ready = reinterpret_cast<int32_t*>(ctl + 528 + 512);                   // [32] producer: flag probe results
 
   const unsigned fullmask = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -138,61 +168,65 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
       // all their consumers have released them), the flag if the probe found it unset, one TMA copy.
       int32_t head = 0, used = 0, oldest = 0;  // lane 0: ring allocator state of this tile
       for (int32_t b0 = 0; b0 < n_ext; b0 += 32) {
-        int4 my = make_int4(0, 0, 0, 0);
-        int32_t ready = 1;
         if (b0 + lane < n_ext) {
-          my = __ldg(reinterpret_cast<const int4*>(a.ext + ext_beg + b0 + lane));
+          const int4 my = __ldg(reinterpret_cast<const int4*>(a.ext + ext_beg + b0 + lane));
+          int32_t ready = 1;
           if ((static_cast<uint32_t>(my.w) >> 16) & kItemWait) {
-            ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my.y) * a.units + u) >= a.gen;
+            ready = ld_flag_relaxed(a.flags + static_cast<int64_t>(my.y) * a.units + u) >= a.gen;
           }
+          p_items[lane] = my;
+          p_ready[lane] = ready;
         }
         __syncwarp();
-        const int nq = min(32, n_ext - b0);
-        for (int q = 0; q < nq; ++q) {
-          const int32_t entry = __shfl_sync(fullmask, my.x, q);
-          const int32_t d = __shfl_sync(fullmask, my.y, q);
-          const uint32_t users = static_cast<uint32_t>(__shfl_sync(fullmask, my.z, q));
-          const uint32_t cf = static_cast<uint32_t>(__shfl_sync(fullmask, my.w, q));
-          const int32_t rdy = __shfl_sync(fullmask, ready, q);
-          if (lane == 0) {
+        if (lane == 0) {
+          const int nq = min(32, n_ext - b0);
+          for (int q = 0; q < nq; ++q) {
+            const int4 my = p_items[q];
+            const int32_t entry = my.x, d = my.y;
+            const uint32_t users = static_cast<uint32_t>(my.z), cf = static_cast<uint32_t>(my.w);
             const int32_t x = b0 + q, gx = ext_base + x;
             const int slot = gx & (kTileSlots - 1);
-            const int nb = (static_cast<int>(cf & 0xffffu) + kTileBoxStep - 1) / kTileBoxStep;  // 1..kTileMaps blocks
-            const bool wrap = head + nb > kTileRingBlocks;  // a copy is contiguous: skip the blocks left at the end
-            const int waste = wrap ? kTileRingBlocks - head : 0;
-            while (x - oldest >= kTileSlots || used + nb + waste > kTileRingBlocks) {
+            const int nb = (static_cast<int>(cf & 0xffu) + kTileBoxStep - 1) / kTileBoxStep;  // 1..kTileMaps blocks
+            const int start = static_cast<int>(cf >> 24);  // ring positions are static (tile_plan.hpp); only the space is awaited
+            const int waste = start < head ? RB - head : 0;  // the planner wrapped: the blocks left at the end are skipped
+            while (x - oldest >= kTileSlots || used + nb + waste > RB) {
               const int os = (ext_base + oldest) & (kTileSlots - 1);
-              while (*reinterpret_cast<volatile int32_t*>(released + os) != p_expect[os]) __nanosleep(32);
+              while (*reinterpret_cast<volatile int32_t*>(released + os) != p_expect[os]) {
+              }
               used -= p_blocks[os];
               ++oldest;
             }
-            if (wrap) head = 0;
-            const int start = head;
-            head += nb;
+            head = start + nb;
             used += nb + waste;
             *reinterpret_cast<volatile int32_t*>(released + slot) = 0;
             p_expect[slot] = __popc(users);
             p_blocks[slot] = nb + waste;
-            slot_blk[slot] = start;
-            if (!rdy) {  // (a flag the probe found set was acquired by another lane; the __syncwarp below the
-              const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;  // probe orders it for this one)
+            // `issued` past gx tells the consumers two things: the slot's previous copy is fully consumed (so the
+            // parity of the mbarrier they are about to wait on is unambiguous) and its release counter is reset.
+            // It does not have to wait for the copy itself: a consumer that comes early sleeps on the mbarrier.
+            __threadfence_block();
+            *issued = gx + 1;
+            if (!p_ready[q]) {
+              const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
               unsigned ns = 32;
-              while (ld_acquire_s32(f) < a.gen) {
+              while (ld_flag_relaxed(f) < a.gen) {
                 __nanosleep(ns);
                 ns = min(ns * 2, 256u);
               }
             }
-            // the pivot row was written through the generic proxy (by this or another SM) and is read by
-            // the async proxy: order the two behind the acquire
+            // The flag is read with a RELAXED gpu-scope load and followed by a generic->async proxy fence,
+            // not by an acquire: the only reader of the data the flag guards is the TMA engine (async proxy,
+            // served by L2, where the owner's fenced stores already are when the flag is visible); no thread of
+            // this kernel reads a pivot row of another tile through the generic proxy, so the L1 invalidation
+            // that ld.acquire.gpu costs (LDG.STRONG + CCTL.IVALL, measured: the top stall of this warp) would
+            // protect nothing.
             asm volatile("fence.proxy.async.global;" ::: "memory");
             mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(nb * kTileBlockDoubles * sizeof(double)));
             tma_load_2d(ring + static_cast<size_t>(start) * kTileBlockDoubles, &a.maps[nb - 1], (u & 3) * kTileScen,
                         static_cast<int32_t>(group_base + entry), full + slot);
-            __threadfence_block();
-            *issued = gx + 1;
           }
-          __syncwarp();
         }
+        __syncwarp();
       }
     } else if (warp < nrows) {
       // ------------------------------------------------------------ consumer: one row of the tile
@@ -208,74 +242,100 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
       for (int32_t j = lane >> 2; j < len; j += 8) {
         cp_async_16(myrow + static_cast<size_t>(j) * kTileScen + (lane & 3) * 2, grow + static_cast<int64_t>(j) * 32 + (lane & 3) * 2);
       }
-      if (e == 0) *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(len) * kTileScen) = make_double2(0.0, 0.0);  // the spare entry
+      *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(len + e) * kTileScen) = make_double2(0.0, 0.0);  // this lane's spare entry
       cp_async_commit_wait_all();
       __syncwarp();
 
+      const uint32_t ring_a = smem_u32(ring), rows_a = smem_u32(rowsm), my2_a = smem_u32(myrow2);
+      const uint32_t issued_a = smem_u32(const_cast<int32_t*>(issued));
+      const uint32_t done_a = smem_u32(const_cast<int32_t*>(done)), uoff_a = smem_u32(uoff);
       int32_t k = 0;  // pivots of this row applied so far
       double2 alpha = make_double2(0.0, 0.0);
       for (int32_t b0 = 0; b0 < ri_cnt; b0 += 32) {
         int4 mine = make_int4(0, 0, 0, 0);
         if (b0 + lane < ri_cnt) mine = __ldg(reinterpret_cast<const int4*>(a.row_items + ri_beg + b0 + lane));
         const int nq = min(32, ri_cnt - b0);
+        // the destinations of an item's first four steps (64 entries) are requested one item ahead
+        uint32_t toff = static_cast<uint32_t>(__shfl_sync(fullmask, mine.x, 0));
+        uint4 wd_next = __ldg(a.tdest + static_cast<size_t>(toff) * kTileEntryLanes + e);
         for (int q = 0; q < nq; ++q) {
-          const uint32_t toff = static_cast<uint32_t>(__shfl_sync(fullmask, mine.x, q));
           const int32_t srcid = __shfl_sync(fullmask, mine.y, q);
           int32_t cnt = __shfl_sync(fullmask, mine.z, q);
           const uint32_t fl = static_cast<uint32_t>(__shfl_sync(fullmask, mine.w, q));
-          // the destinations of the first four iterations (64 entries), requested before the waits below
           const uint4* __restrict__ tw = a.tdest + static_cast<size_t>(toff) * kTileEntryLanes + e;
-          uint4 wd = __ldg(tw);
+          uint4 wd = wd_next;
+          if (q + 1 < nq) {
+            toff = static_cast<uint32_t>(__shfl_sync(fullmask, mine.x, q + 1));
+            wd_next = __ldg(a.tdest + static_cast<size_t>(toff) * kTileEntryLanes + e);
+          }
           const bool internal = (fl & kItemInternal) != 0;
-          const double* src;
+          uint32_t src_a;
           int slot = 0;
           if (internal) {
-            while (done[srcid] == 0) __nanosleep(32);
+            while (lds32_volatile(done_a + 4 * srcid) == 0) {
+              if (B200LU_TILE_SPIN_NS) __nanosleep(B200LU_TILE_SPIN_NS);
+            }
             __threadfence_block();
-            src = rowsm + static_cast<size_t>(uoff[srcid]) * kTileScen;
+            src_a = rows_a + static_cast<uint32_t>(lds32_volatile(uoff_a + 4 * srcid)) * (kTileScen * 8);
           } else {
             const int32_t gx = ext_base + srcid;
             slot = gx & (kTileSlots - 1);
-            while (*issued <= gx) __nanosleep(64);
+            while (lds32_volatile(issued_a) <= gx) {
+              if (B200LU_TILE_SPIN_NS) __nanosleep(B200LU_TILE_SPIN_NS);
+            }
             mbar_wait(full + slot, static_cast<uint32_t>(gx / kTileSlots) & 1u);
-            src = ring + static_cast<size_t>(slot_blk[slot]) * kTileBlockDoubles;
+            src_a = ring_a + ((fl >> 8) & 0xffu) * (kTileBlockDoubles * 8);
           }
-          const double* sl = src + e * kTileScen + 2 * sp;
+          uint32_t sl_a = src_a + e * (kTileScen * 8) + sp * 16;
           if (fl & kItemFirst) {
-            const double2 aik = *reinterpret_cast<const double2*>(myrow2 + static_cast<size_t>(k) * kTileScen);
-            const double2 udd = *reinterpret_cast<const double2*>(src + 2 * sp);
+            const double2 aik = lds128(my2_a + k * (kTileScen * 8));
+            const double2 udd = lds128(src_a + sp * 16);
             alpha.x = aik.x / udd.x;  // src/numeric.cpp:40
             alpha.y = aik.y / udd.y;
-            sl += kTileScen;  // the diagonal is entry 0 of a first chunk
+            sl_a += kTileScen * 8;  // the diagonal is entry 0 of a first chunk
             --cnt;
           }
           const int32_t iters = (cnt + kTileIter - 1) / kTileIter;
           for (int32_t g0 = 0; g0 < iters; g0 += kTileGroup) {
-            const uint4 w = wd;
+            const uint32_t ww[4] = {wd.x, wd.y, wd.z, wd.w};
             if (g0 + kTileGroup < iters) wd = __ldg(tw + static_cast<size_t>(g0 / kTileGroup + 1) * kTileEntryLanes);
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int i4 = 0; i4 < kTileGroup; ++i4) {
-              if (g0 + i4 < iters) {  // warp-uniform
-                const double* up = sl + static_cast<size_t>(g0 + i4) * kTileIter * kTileScen;
-                const double2 u0 = *reinterpret_cast<const double2*>(up);
-                const double2 u1 = *reinterpret_cast<const double2*>(up + kTileEntryLanes * kTileScen);
-                double2* p0 = reinterpret_cast<double2*>(myrow2 + (ww[i4] & 0xffffu) * kTileScen);
-                double2* p1 = reinterpret_cast<double2*>(myrow2 + (ww[i4] >> 16) * kTileScen);
-                double2 a0 = *p0, a1 = *p1;
+            for (int i2 = 0; i2 < kTileGroup; i2 += 2) {  // two steps at a time: 8 loads in flight, then the arithmetic, then 4 stores
+              if (g0 + i2 < iters) {  // warp-uniform
+                const bool two = g0 + i2 + 1 < iters;
+                const uint32_t up = sl_a + static_cast<uint32_t>(g0 + i2) * (kTileIter * kTileScen * 8);
+                const uint32_t p0 = my2_a + (ww[i2] & 0xffffu) * (kTileScen * 8), p1 = my2_a + (ww[i2] >> 16) * (kTileScen * 8);
+                const uint32_t p2 = my2_a + (ww[i2 + 1] & 0xffffu) * (kTileScen * 8), p3 = my2_a + (ww[i2 + 1] >> 16) * (kTileScen * 8);
+                const double2 u0 = lds128(up), u1 = lds128(up + kTileEntryLanes * kTileScen * 8);
+                double2 a0 = lds128(p0), a1 = lds128(p1);
+                double2 u2 = make_double2(0.0, 0.0), u3 = u2, a2 = u2, a3 = u2;
+                if (two) {
+                  u2 = lds128(up + kTileIter * kTileScen * 8);
+                  u3 = lds128(up + (kTileIter + kTileEntryLanes) * kTileScen * 8);
+                  a2 = lds128(p2);
+                  a3 = lds128(p3);
+                }
                 a0.x = __dsub_rn(a0.x, __dmul_rn(alpha.x, u0.x));  // src/numeric.cpp:44
                 a0.y = __dsub_rn(a0.y, __dmul_rn(alpha.y, u0.y));
                 a1.x = __dsub_rn(a1.x, __dmul_rn(alpha.x, u1.x));
                 a1.y = __dsub_rn(a1.y, __dmul_rn(alpha.y, u1.y));
-                *p0 = a0;
-                *p1 = a1;
+                sts128(p0, a0);
+                sts128(p1, a1);
+                if (two) {
+                  a2.x = __dsub_rn(a2.x, __dmul_rn(alpha.x, u2.x));
+                  a2.y = __dsub_rn(a2.y, __dmul_rn(alpha.y, u2.y));
+                  a3.x = __dsub_rn(a3.x, __dmul_rn(alpha.x, u3.x));
+                  a3.y = __dsub_rn(a3.y, __dmul_rn(alpha.y, u3.y));
+                  sts128(p2, a2);
+                  sts128(p3, a3);
+                }
               }
             }
           }
           __syncwarp();  // every lane's updates are in shared memory before the next pivot reads them
           if (!internal && lane == 0) atomicAdd(released + slot, 1);
           if (fl & kItemLast) {
-            if (e == 0) *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(k) * kTileScen) = alpha;  // l_id, src/numeric.cpp:41
+            if (e == 0) sts128(my2_a + k * (kTileScen * 8), alpha);  // l_id, src/numeric.cpp:41
             ++k;
           }
         }

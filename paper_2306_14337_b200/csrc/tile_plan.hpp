@@ -23,12 +23,12 @@ constexpr int kTileEntryLanes = 8;      // lanes = 8 entry lanes x 4 scenario pa
 constexpr int kTileChunk = 96;          // most entries of a pivot row fetched by one TMA copy
 constexpr int kTileBoxStep = 16;        // TMA box heights: 16, 32, ..., kTileChunk; also the ring's block size (entries)
 constexpr int kTileMaps = kTileChunk / kTileBoxStep;
-constexpr int kTileRingBlocks = 32;     // ring of 32 blocks x 16 entries x 64 bytes = 32 KB of staged pivot rows
 constexpr int kTileSlots = 16;          // pivot-row copies in flight (mbarriers)
 constexpr int kTileMaxRows = 16;        // rows (consumer warps) of a tile
 constexpr int kTileIter = 16;           // entries of a pivot row applied per inner-loop iteration (8 lanes x 2)
 constexpr int kTileGroup = 4;           // iterations whose destinations one 16-byte load per lane brings in
 constexpr int kTileGroupEntries = kTileIter * kTileGroup;  // 64 destination slots = 128 bytes per group
+constexpr int kTileSpare = kTileEntryLanes;  // spare entries behind a row in shared memory: one per entry lane
 
 struct TileRow {       // 32 bytes, one per row of a tile
   int32_t row;         // row index
@@ -37,8 +37,8 @@ struct TileRow {       // 32 bytes, one per row of a tile
   int32_t nl;          // strict-lower entries = pivots; the diagonal is entry nl
   int32_t ri_beg;      // its RowItems
   int32_t ri_cnt;
-  int32_t smem_off;    // entry offset of the row inside the tile's shared-memory block (len + 1 entries:
-  int32_t pad;         //   the last one absorbs the padding lanes' updates)
+  int32_t smem_off;    // entry offset of the row inside the tile's shared-memory block (len + kTileSpare
+  int32_t pad;         //   entries: the spare ones absorb the padding lanes' updates, one per entry lane)
 };
 struct TileMeta {      // 16 bytes
   int32_t row_beg, nrows;
@@ -49,13 +49,13 @@ struct ExtItem {       // 16 bytes: what the producer fetches
   int32_t entry;       // first entry of the chunk in values[] (the pivot row's diagonal for a first chunk)
   int32_t d;           // pivot row (ready flag)
   uint32_t users;      // rows of the tile that consume it (bit mask)
-  uint32_t cnt_flags;  // entries of the chunk (a first chunk counts the diagonal) | kItem* << 16
+  uint32_t cnt_flags;  // entries of the chunk (a first chunk counts the diagonal) | kItem* << 16 | first ring block << 24
 };
 struct RowItem {       // 16 bytes: one pivot-row chunk as ONE row of the tile consumes it
   uint32_t tdest_off;  // its destination slice in the tile destination table, in groups (128 bytes each)
   uint32_t src;        // external: index of the ExtItem within the tile; internal: which row of the tile
   uint32_t cnt;        // entries of the chunk (a first chunk counts the diagonal)
-  uint32_t flags;      // kItem*
+  uint32_t flags;      // kItem* | first ring block of the staged copy << 8 (external)
 };
 static_assert(sizeof(TileRow) == 32 && sizeof(TileMeta) == 16 && sizeof(ExtItem) == 16 && sizeof(RowItem) == 16,
               "device record layout");
@@ -70,8 +70,8 @@ struct TilePlan {
   // 16t + e and 16t + 8 + e. A group is four iterations: lane e finds the eight destination offsets
   // (entry index inside the target row) it needs for them in ONE 16-byte word:
   //     tdest[(tdest_off + t / 4) * 64 + 8 e + 2 (t % 4) + j]   for entry 16 t + 8 j + e.
-  // Slots past the chunk's end point at the row's spare entry (offset len): the inner loop needs no
-  // predicates.
+  // Slots past the chunk's end point at the spare entry of their lane (offset len + e): the inner loop
+  // needs no predicates, and no two threads ever write one address.
   std::vector<uint16_t> tdest;
   int64_t rows_smem_entries = 0; // largest tile, in entries (x 64 bytes), spare entries included
   int64_t fetched_entries = 0;   // sum of external item sizes (what TMA moves per unit)
@@ -100,7 +100,7 @@ inline int32_t tile_dest_slot(int32_t t) {
 // tail row); every other row is final before the tiled launch starts. `cap_entries`: shared-memory
 // capacity of a tile in entries. Returns "" or the reason the pattern cannot be tiled.
 inline std::string build_tile_plan(const Schedule& S, const std::vector<int32_t>& tail_rows, int rows_per_tile,
-                                   int64_t cap_entries, TilePlan& plan) {
+                                   int64_t cap_entries, TilePlan& plan, int ring_blocks = 32) {
   plan = TilePlan{};
   const int64_t n = S.n;
   const int R = std::min(rows_per_tile, kTileMaxRows);
@@ -115,13 +115,13 @@ inline std::string build_tile_plan(const Schedule& S, const std::vector<int32_t>
     int64_t used = 0;
     while (b0 < tail_rows.size() && t.nrows < R) {
       const int32_t i = tail_rows[b0];
-      const int64_t len = S.row_ptr[i + 1] - S.row_ptr[i] + 1;  // + the spare entry
-      if (len > cap_entries) return "row " + std::to_string(i) + " (" + std::to_string(len - 1) + " entries) exceeds a tile's shared memory";
+      const int64_t len = S.row_ptr[i + 1] - S.row_ptr[i] + kTileSpare;  // + the spare entries
+      if (len > cap_entries) return "row " + std::to_string(i) + " (" + std::to_string(len - kTileSpare) + " entries) exceeds a tile's shared memory";
       if (used + len > cap_entries) break;
       TileRow tr{};
       tr.row = i;
       tr.lo = S.row_ptr[i];
-      tr.len = static_cast<int32_t>(len - 1);
+      tr.len = static_cast<int32_t>(len - kTileSpare);
       tr.nl = S.diag[i] - S.row_ptr[i];
       tr.smem_off = static_cast<int32_t>(used);
       plan.rows.push_back(tr);
@@ -148,6 +148,7 @@ inline std::string build_tile_plan(const Schedule& S, const std::vector<int32_t>
     }
     std::sort(piv.begin(), piv.end());
     int32_t last_pred = -1;
+    int32_t ring_head = 0;  // the staging ring is allocated in order, from block 0 in every tile: positions are static
     for (size_t q = 0; q < piv.size();) {
       const int32_t d = piv[q].first;
       const size_t q0 = q;
@@ -174,6 +175,10 @@ inline std::string build_tile_plan(const Schedule& S, const std::vector<int32_t>
         uint32_t src = static_cast<uint32_t>(owner);
         if (!internal) {
           src = static_cast<uint32_t>(ext[b].size());
+          const int32_t nb = static_cast<int32_t>((cnt + kTileBoxStep - 1) / kTileBoxStep);
+          if (ring_head + nb > ring_blocks) ring_head = 0;  // a copy is contiguous: the blocks left at the end are skipped
+          fl |= static_cast<uint32_t>(ring_head) << 8;      // first ring block of the copy
+          ring_head += nb;
           ext[b].push_back(ExtItem{static_cast<int32_t>(dd + c0), d, users, static_cast<uint32_t>(cnt) | (fl << 16)});
           plan.fetched_entries += cnt;
         }
@@ -197,8 +202,11 @@ inline std::string build_tile_plan(const Schedule& S, const std::vector<int32_t>
       const int32_t groups = std::max(1, (cu + kTileGroupEntries - 1) / kTileGroupEntries);  // >= 1: the first word is always loaded
       if (plan.tdest.size() / kTileGroupEntries + groups >= (uint64_t{1} << 32)) return "tile destination table too large";
       ri.tdest_off = static_cast<uint32_t>(plan.tdest.size() / kTileGroupEntries);
-      plan.tdest.resize(plan.tdest.size() + static_cast<size_t>(groups) * kTileGroupEntries, static_cast<uint16_t>(tr.len));
+      plan.tdest.resize(plan.tdest.size() + static_cast<size_t>(groups) * kTileGroupEntries);
       uint16_t* slice = plan.tdest.data() + static_cast<size_t>(ri.tdest_off) * kTileGroupEntries;
+      for (int32_t x = 0; x < groups * kTileGroupEntries; ++x) {  // padding: the spare entry of the lane that reads the slot
+        slice[x] = static_cast<uint16_t>(tr.len + (x % kTileGroupEntries) / 8);
+      }
       int32_t pos = k + 1;   // destinations ascend with the pivot row's columns
       for (int32_t t = 0; t < cu; ++t) {
         const int32_t j = S.col[dd + 1 + c + t];
@@ -250,7 +258,7 @@ inline int64_t emulate_tile_plan(const Schedule& S, const TilePlan& plan, double
     for (int r = 0; r < tm.nrows; ++r) {
       const TileRow& tr = plan.rows[tm.row_beg + r];
       row[r].assign(values + tr.lo, values + tr.lo + tr.len);
-      row[r].push_back(0.0);  // the spare entry
+      row[r].resize(tr.len + kTileSpare, 0.0);  // the spare entries
     }
     for (int r = 0; r < tm.nrows; ++r) {  // internal pivots are rows of smaller index: already final
       const TileRow& tr = plan.rows[tm.row_beg + r];
@@ -286,8 +294,8 @@ inline int64_t emulate_tile_plan(const Schedule& S, const TilePlan& plan, double
               const int32_t t = it * kTileIter + kTileEntryLanes * j + e;
               const int32_t ds = slice[tile_dest_slot(t)];
               const double u = t < avail ? src[t] : 12345.0;  // the device reads whatever follows; it lands in the spare entry
-              if (t >= cu && ds != tr.len) return -4;
-              if (ds > tr.len) return -4;
+              if (t >= cu && ds != tr.len + e) return -4;  // padding goes to the lane's own spare entry
+              if (t < cu && ds >= tr.len) return -4;
               const double prod = alpha * u;
               row[r][ds] = row[r][ds] - prod;
             }

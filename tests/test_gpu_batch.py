@@ -234,3 +234,107 @@ def test_batch_classic_refine_matches_the_oracle_per_scenario():
         assert len(outcomes[s].residual_history) == len(hist_ref)
     # identity preconditioner on a diagonal system converges only where the diagonal is 1 (test_refine.cpp:148-159 style)
     f.close()
+
+
+@pytest.fixture
+def tiles_env():
+    """Selects the trailing-part kernel of the next BatchedFactors (the choice is made at create time)."""
+    old = os.environ.get("B200LU_BATCH_TILES")
+
+    def choose(v):
+        if v is None:
+            os.environ.pop("B200LU_BATCH_TILES", None)
+        else:
+            os.environ["B200LU_BATCH_TILES"] = v
+
+    yield choose
+    choose(old)
+
+
+@pytest.mark.parametrize("name", ["kkt_small", "kkt_small_mc64", "random_sparse_120_plain"])
+@pytest.mark.parametrize("mode,batch", [("1", 7), ("1", 40), ("0", 7), ("0", 40), (None, 9), (None, 130)])
+def test_both_trailing_kernels_are_bitwise_exact(tiles_env, name, mode, batch):
+    """The trailing part of the refactorization runs either in the tiled kernel (rows resident in shared
+    memory, TMA-staged pivot rows, csrc/tile.cuh) or in the row-blocked one (L2 reductions, csrc/batch.cuh):
+    forced each way and left to the default (tiles up to 96 scenarios), every scenario's L/U values must be
+    the oracle's bit for bit, twice in a row (generation flags, run-to-run determinism)."""
+    fx = golden_fixture(name)
+    vals, rhs = _scenarios(fx, batch)
+    tiles_env(mode)
+    f = BatchedFactors(fx.sym, batch)
+    try:
+        info = f.info
+        if mode is not None:
+            assert info["tiled"] == int(mode)
+        else:
+            assert info["tiled"] == (1 if batch <= 96 else 0)
+        for rep in range(2):
+            f.refactorize(vals)
+            for s in sorted({0, 1, batch // 2, batch - 1}):
+                ref, failed = fx.oracle.factorize(vals[s])
+                assert failed == -1 and np.array_equal(f.values(s), ref), (rep, s)
+        x = f.solve_system(rhs)
+        s = batch - 1
+        assert np.array_equal(x[s], fx.oracle.solve_system(fx.oracle.factorize(vals[s])[0], rhs[s])[0])
+    finally:
+        f.close()
+
+
+def test_tiled_kernel_zero_pivot_and_pivot_floor(tiles_env):
+    """eliminate's pivot check (src/numeric.cpp:48-55) in the tiled kernel: the lowest failing row per scenario,
+    the other scenarios unaffected and valid."""
+    fx = golden_fixture("kkt_small")
+    batch = 6
+    vals, _ = _scenarios(fx, batch)
+    tiles_env("1")
+    f = BatchedFactors(fx.sym, batch, rlu.FactorOptions(pivot_floor=1e300))
+    try:
+        assert f.info["tiled"] == 1
+        failed = f.refactorize(vals, raise_on_zero_pivot=False)
+        for s in range(batch):
+            ref, ref_failed = fx.oracle.factorize(vals[s], pivot_floor=1e300)
+            assert failed[s] == ref_failed and not f.valid(s)
+            assert np.array_equal(f.values(s), ref)
+    finally:
+        f.close()
+
+
+@needs_ref
+def test_tiled_kernel_chunks_long_pivot_rows(tiles_env):
+    """A dense 150 x 150 matrix has pivot rows of up to 150 entries: longer than one staging copy (96 entries),
+    so they are staged and applied in chunks."""
+    rng = np.random.default_rng(7)
+    M = rng.uniform(-1.0, 1.0, (150, 150)) + 150.0 * np.eye(150)
+    fx = dense_fixture(M)
+    tiles_env("1")
+    f = BatchedFactors(fx.sym, 3)
+    try:
+        assert f.info["tiled"] == 1
+        vals = np.stack([fx.values[0], 2.0 * fx.values[0], 0.5 * fx.values[0]])
+        f.refactorize(vals)
+        for s in range(3):
+            assert np.array_equal(f.values(s), fx.oracle.factorize(vals[s])[0])
+    finally:
+        f.close()
+
+
+@needs_ref
+def test_pattern_the_tiled_kernel_cannot_take_keeps_the_row_blocked_one(tiles_env):
+    """An arrow matrix whose last row holds 3 700 entries does not fit a tile's shared memory (64 bytes per
+    entry): the handle keeps the row-blocked kernel and stays exact."""
+    n = 3700
+    rng = np.random.default_rng(11)
+    M = np.diag(rng.uniform(2.0, 3.0, n))
+    M[-1, :-1] = rng.uniform(-1e-3, 1e-3, n - 1)
+    M[:-1, -1] = rng.uniform(-1e-3, 1e-3, n - 1)
+    fx = dense_fixture(M)
+    tiles_env("1")
+    f = BatchedFactors(fx.sym, 2)
+    try:
+        assert f.info["tiled"] == 0
+        vals = np.stack([fx.values[0], 2.0 * fx.values[0]])
+        f.refactorize(vals)
+        for s in range(2):
+            assert np.array_equal(f.values(s), fx.oracle.factorize(vals[s])[0])
+    finally:
+        f.close()
