@@ -199,6 +199,16 @@ b200lu_status b200lu_refine_classic(b200lu_handle* h, const double* b, const dou
                                     double* x_out, int on_device, int use_preconditioner,
                                     const b200lu_refine_config* cfg, b200lu_refine_outcome* outcome);
 
+/* cgs2_orthonormalize (include/rlu/refine.hpp:25-35, src/refine.cpp:8-26): two full Gram-Schmidt passes of
+ * v against the k orthonormal vectors basis[j] ([k][n], contiguous), then normalisation. coefficients_out[k]
+ * (host): the combined projection coefficients; vector_out[n]: the normalised remainder (the unnormalised one
+ * on breakdown); *norm_out: the remainder's norm before normalisation; *breakdown_out: 1 when that norm is at
+ * most 1e-300. k may not exceed the handle's refine_capacity. basis / v / vector_out are host or device
+ * pointers as `on_device` says. */
+b200lu_status b200lu_cgs2_orthonormalize(b200lu_handle* h, int64_t k, const double* basis, const double* v,
+                                         int on_device, double* coefficients_out, double* vector_out,
+                                         double* norm_out, int* breakdown_out);
+
 b200lu_status b200lu_get_stats(const b200lu_handle* h, b200lu_stats* out);
 /* Host-only (needs no device): validates a symbolic view and derives the device schedule the
  * way b200lu_create does — the level orders that replace SyncFreeScheduler's ascending claim
@@ -330,8 +340,10 @@ b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on
  * a third stream. Host buffers should be page-locked (cudaHostRegister / pinned allocation) for the copies
  * to overlap. Typical loop:
  *     stage_inputs(v[0], b[0]);
- *     for k: refactorize_staged(); if (k + 1 < K) stage_inputs(v[k+1], b[k+1]); solve_refine_staged(.., x[k], ..);
+ *     for k: if (k + 1 < K) stage_inputs(v[k+1], b[k+1]); refactorize_staged(); solve_refine_staged(.., x[k], ..);
  *     staged_wait();                  // x[k] may be read only after staged_wait (or after the next-but-one call)
+ * Staged inputs are consumed in the order they were staged (two staging sets: at most two batches may be
+ * staged and unconsumed; a third stage_inputs is refused).
  * stage_inputs: [batch][nnz_source] values and/or [batch][n] right-hand sides (either may be NULL to keep the
  * previous one); returns at once. refactorize_staged = reset_values + factorize_scattered on the staged values
  * (src/numeric.cpp:70-79). solve_refine_staged = solve_system (src/trisolve.cpp:90-119) on the staged

@@ -4,16 +4,16 @@ Drop-in for the reference library's numeric / triangular-solve / refinement entr
 reference's host-side symbolic analysis is consumed as-is. See include/b200lu.h for the C ABI and
 DESIGN.md for the kernels.
 """
-from .solver import (CsrMatrix, DeviceError, DimensionError, Error, FactorOptions, NumericFactors,
+from .solver import (Cgs2Result, CsrMatrix, DeviceError, DimensionError, Error, FactorOptions, NumericFactors,
                      PatternMismatchError, RefineConfig, RefineOutcome, SymbolicFactors,
-                     ZeroPivotError, classic_refine, factorize, factorize_scattered, fgmres_refine,
+                     ZeroPivotError, cgs2_orthonormalize, classic_refine, factorize, factorize_scattered, fgmres_refine,
                      kkt_bind, kkt_update, lower_solve, refactorize, relative_residual, reset_values, scatter_values,
                      solve_system, spmv, upper_solve)
 
 __all__ = [
-    "CsrMatrix", "DeviceError", "DimensionError", "Error", "FactorOptions", "NumericFactors",
+    "Cgs2Result", "CsrMatrix", "DeviceError", "DimensionError", "Error", "FactorOptions", "NumericFactors",
     "PatternMismatchError", "RefineConfig", "RefineOutcome", "SymbolicFactors", "ZeroPivotError",
-    "classic_refine", "factorize", "factorize_scattered", "fgmres_refine", "kkt_bind", "kkt_update", "lower_solve",
+    "cgs2_orthonormalize", "classic_refine", "factorize", "factorize_scattered", "fgmres_refine", "kkt_bind", "kkt_update", "lower_solve",
     "refactorize", "relative_residual", "reset_values", "scatter_values", "solve_system", "spmv",
     "upper_solve",
 ]

@@ -83,6 +83,7 @@ EXPORTS = {
                                    C.POINTER(RefineOutcome)]),
     "b200lu_refine_classic": (i32, [vp, vp, vp, vp, i32, i32, C.POINTER(RefineConfig),
                                     C.POINTER(RefineOutcome)]),
+    "b200lu_cgs2_orthonormalize": (i32, [vp, i64, vp, vp, i32, vp, vp, C.POINTER(dbl), C.POINTER(i32)]),
     "b200lu_get_stats": (i32, [vp, C.POINTER(Stats)]),
     "b200lu_schedule_probe": (i32, [C.POINTER(SymbolicView), C.POINTER(Stats), vp, vp, vp, C.c_char_p, i32]),
     "b200lu_set_timing": (i32, [vp, i32]),

@@ -304,6 +304,60 @@ class BatchedFactors:
                                       bool(o.converged)) for s, o in enumerate(ocs)]
         return out, outcomes
 
+    # -- staged (pipelined) submission ------------------------------------------
+    def _host_ptr(self, a, width, what):
+        """Host buffer (numpy array or CPU torch tensor, ideally page-locked) -> (pointer, keepalive)."""
+        if a is None:
+            return None, None
+        if hasattr(a, "data_ptr") and not rlu._is_device_tensor(a):  # CPU torch tensor (pin_memory() keeps copies async)
+            import torch
+            if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != self.batch * width:
+                raise rlu.DimensionError(f"{what}: expected a contiguous float64 [{self.batch}, {width}] tensor")
+            return a.data_ptr(), a
+        if rlu._is_device_tensor(a):
+            raise rlu.Error(f"{what}: the staged calls take HOST buffers")
+        h = np.ascontiguousarray(a, dtype=np.float64)
+        if h.size != self.batch * width:
+            raise rlu.DimensionError(f"{what}: expected [{self.batch}, {width}] values, got {h.size}")
+        return h.ctypes.data, h
+
+    def stage_inputs(self, values=None, rhs=None):
+        """Starts the host-to-device copy of the NEXT batch's values and/or right-hand sides on the handle's
+        copy stream and returns at once (b200lu_batch_stage_inputs). The buffers must stay alive and
+        unchanged until the matching *_staged call has been issued and the device has caught up."""
+        pv, kv = self._host_ptr(values, len(self.symbolic.scatter_map), "stage_inputs")
+        pr, kr = self._host_ptr(rhs, self.symbolic.n, "stage_inputs")
+        self._staged_keep = getattr(self, "_staged_keep", [])[-4:] + [kv, kr]
+        self._check(_capi.lib().b200lu_batch_stage_inputs(self._h, pv, pr))
+
+    def refactorize_staged(self, raise_on_zero_pivot=True):
+        """refactorize (src/numeric.cpp:70-73) on the staged values."""
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        st = _capi.lib().b200lu_batch_refactorize_staged(self._h, failed.ctypes.data)
+        if st == _capi.ZERO_PIVOT and not raise_on_zero_pivot:
+            return failed
+        self._check(st, failed)
+        return failed
+
+    def solve_refine_staged(self, out, config: rlu.RefineConfig | None = None, refine: bool = True):
+        """solve_system on the staged right-hand sides, then fgmres_refine from that solution; the result is
+        copied into the host buffer `out` ([batch, n]) asynchronously: read it after staged_wait().
+        Returns the refinement outcomes (their .x is a view of `out`)."""
+        po, keep = self._host_ptr(out, self.symbolic.n, "solve_refine_staged")
+        config = config or rlu.RefineConfig()
+        cfg = _capi.RefineConfig(config.max_iterations, config.tolerance)
+        ocs = (_capi.RefineOutcome * self.batch)()
+        failed = np.full(self.batch, -1, dtype=np.int64)
+        self._check(_capi.lib().b200lu_batch_solve_refine_staged(self._h, 1 if refine else 0, C.byref(cfg), po,
+                                                                 C.cast(ocs, C.c_void_p), failed.ctypes.data), failed)
+        if not refine:
+            return []
+        return [rlu.RefineOutcome(out[s], int(o.iterations), list(o.residual_history[:o.history_len]), bool(o.converged))
+                for s, o in enumerate(ocs)]
+
+    def staged_wait(self):
+        self._check(_capi.lib().b200lu_batch_staged_wait(self._h))
+
     # -- reporting -------------------------------------------------------------
     @property
     def info(self) -> dict:

@@ -1243,6 +1243,60 @@ b200lu_status b200lu_refine_classic(b200lu_handle* h, const double* b, const dou
   return refine_common(h, b, x0, x_out, on_device, use_preconditioner, cfg, outcome, false);
 }
 
+// cgs2_orthonormalize (src/refine.cpp:8-26): two passes of "h = dot(basis_j, v); coefficient_j += h;
+// v -= h * basis_j" over the basis, then the norm; breakdown when norm <= 1e-300, otherwise v / norm.
+// The device kernels are the ones fgmres_refine uses for its orthogonalisation step.
+b200lu_status b200lu_cgs2_orthonormalize(b200lu_handle* h, int64_t k, const double* basis, const double* v, int on_device,
+                                         double* coefficients_out, double* vector_out, double* norm_out, int* breakdown_out) {
+  if (!h || k < 0 || (k > 0 && (!basis || !coefficients_out)) || (h->n && (!v || !vector_out)) || !norm_out || !breakdown_out) {
+    return B200LU_INVALID_ARGUMENT;
+  }
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (k > h->refine_capacity) {
+    h->last_error = "cgs2_orthonormalize: more basis vectors than the handle's refine_capacity";
+    return B200LU_INVALID_ARGUMENT;
+  }
+  const int64_t n = h->n;
+  const int32_t n32 = static_cast<int32_t>(n);
+  const int nb = blocks_for(n, 256);
+  *norm_out = 0.0;
+  *breakdown_out = 1;
+  if (n == 0) return B200LU_OK;
+  const cudaMemcpyKind in_kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (k > 0) CU_TRY(h, cudaMemcpyAsync(h->d_V, basis, static_cast<size_t>(k) * n * sizeof(double), in_kind, h->stream));
+  CU_TRY(h, cudaMemcpyAsync(h->d_wv, v, static_cast<size_t>(n) * sizeof(double), in_kind, h->stream));
+  CU_TRY(h, cudaMemsetAsync(h->d_scal + kSlotCoef, 0, static_cast<size_t>(std::max<int64_t>(k, 1)) * sizeof(double), h->stream));
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int64_t j = 0; j < k; ++j) {
+      ST_TRY(launch_dot(h, h->d_V + j * n, h->d_wv, kSlotH));
+      {
+        PhaseScope ps(h, B200LU_PHASE_VECTOR);
+        project_out_kernel<<<nb, 256, 0, h->stream>>>(n32, h->d_scal + kSlotH, h->d_scal + kSlotCoef + j, h->d_V + j * n, h->d_wv);
+      }
+      ST_TRY(check_launch(h, "project_out_kernel"));
+    }
+  }
+  ST_TRY(launch_dot(h, h->d_wv, h->d_wv, kSlotNorm));
+  ST_TRY(read_scalars(h, kSlotNorm, static_cast<int>(kSlotCoef + k - kSlotNorm)));
+  const double norm = std::sqrt(h->h_scal[kSlotNorm]);
+  for (int64_t j = 0; j < k; ++j) coefficients_out[j] = h->h_scal[kSlotCoef + j];
+  *norm_out = norm;
+  *breakdown_out = norm <= 1e-300 ? 1 : 0;
+  const double* result = h->d_wv;  // on breakdown the vector is unspecified (include/rlu/refine.hpp:27): the remainder
+  if (!*breakdown_out) {
+    {
+      PhaseScope ps(h, B200LU_PHASE_VECTOR);
+      divide_kernel<<<nb, 256, 0, h->stream>>>(n32, norm, h->d_wv, h->d_r);
+    }
+    ST_TRY(check_launch(h, "divide_kernel"));
+    result = h->d_r;
+  }
+  CU_TRY(h, cudaMemcpyAsync(vector_out, result, static_cast<size_t>(n) * sizeof(double),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  return B200LU_OK;
+}
+
 b200lu_status b200lu_get_stats(const b200lu_handle* h, b200lu_stats* out) {
   if (!h || !out) return B200LU_INVALID_ARGUMENT;
   out->n = h->n;

@@ -127,8 +127,9 @@ struct b200lu_batch {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_vals_used[2] = {nullptr, nullptr}, ev_rhs_used[2] = {nullptr, nullptr},
               ev_x[2] = {nullptr, nullptr}, ev_x_out[2] = {nullptr, nullptr};
   double *d_stage_vals[2] = {nullptr, nullptr}, *d_stage_rhs[2] = {nullptr, nullptr}, *d_stage_x[2] = {nullptr, nullptr};
-  int stage_fill = 0, stage_cur = -1;   // buffer the next stage_inputs fills; buffer holding the staged inputs
-  bool staged_vals = false, staged_rhs = false, staged_ready = false;
+  int stage_fill = 0;                    // buffer the next stage_inputs fills
+  std::vector<int> vals_queue, rhs_queue;  // staged buffers not yet consumed, oldest first (at most two each)
+  bool staged_ready = false;
 
   int64_t alloc_events = 0, device_bytes = 0;
   uint64_t launches = 0;
@@ -1566,6 +1567,18 @@ b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_valu
   CU_TRY(h, cudaSetDevice(h->device));
   ST_TRY(stage_setup(h));
   const int buf = h->stage_fill;
+  for (int q : h->vals_queue) {
+    if (q == buf && host_values) {
+      h->last_error = "stage_inputs: both staging buffers hold values that have not been consumed (refactorize_staged)";
+      return B200LU_INVALID_ARGUMENT;
+    }
+  }
+  for (int q : h->rhs_queue) {
+    if (q == buf && host_rhs) {
+      h->last_error = "stage_inputs: both staging buffers hold right-hand sides that have not been consumed (solve_refine_staged)";
+      return B200LU_INVALID_ARGUMENT;
+    }
+  }
   // the buffer's previous contents must have been consumed by the compute stream
   CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_vals_used[buf], 0));
   CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_rhs_used[buf], 0));
@@ -1578,9 +1591,8 @@ b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_valu
                               cudaMemcpyHostToDevice, h->copy_in));
   }
   CU_TRY(h, cudaEventRecord(h->ev_in[buf], h->copy_in));
-  h->staged_vals = host_values != nullptr;
-  h->staged_rhs = host_rhs != nullptr;
-  h->stage_cur = buf;
+  if (host_values) h->vals_queue.push_back(buf);
+  if (host_rhs) h->rhs_queue.push_back(buf);
   h->stage_fill = buf ^ 1;
   return B200LU_OK;
 }
@@ -1588,11 +1600,12 @@ b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_valu
 b200lu_status b200lu_batch_refactorize_staged(b200lu_batch* h, int64_t* failed_rows) {
   if (!h) return B200LU_INVALID_ARGUMENT;
   CU_TRY(h, cudaSetDevice(h->device));
-  if (h->stage_cur < 0 || !h->staged_vals) {
+  if (h->vals_queue.empty()) {
     h->last_error = "refactorize_staged: no staged values (call b200lu_batch_stage_inputs first)";
     return B200LU_INVALID_ARGUMENT;
   }
-  const int buf = h->stage_cur;
+  const int buf = h->vals_queue.front();
+  h->vals_queue.erase(h->vals_queue.begin());
   CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[buf], 0));
   std::fill(h->valid.begin(), h->valid.end(), 0);
   h->have_values = true;
@@ -1605,7 +1618,6 @@ b200lu_status b200lu_batch_refactorize_staged(b200lu_batch* h, int64_t* failed_r
     }
   }
   CU_TRY(h, cudaEventRecord(h->ev_vals_used[buf], h->stream));
-  h->staged_vals = false;
   ST_TRY(launch_scatter(h));
   return launch_factor(h, failed_rows);
 }
@@ -1615,7 +1627,7 @@ b200lu_status b200lu_batch_solve_refine_staged(b200lu_batch* h, int refine, cons
   for (int32_t s = 0; h && failed_rows && s < h->batch; ++s) failed_rows[s] = -1;
   if (!h || (!host_x_out && h->n) || (refine && !outcomes)) return B200LU_INVALID_ARGUMENT;
   CU_TRY(h, cudaSetDevice(h->device));
-  if (h->stage_cur < 0 || !h->staged_rhs) {
+  if (h->rhs_queue.empty()) {
     h->last_error = "solve_refine_staged: no staged right-hand sides (call b200lu_batch_stage_inputs first)";
     return B200LU_INVALID_ARGUMENT;
   }
@@ -1627,11 +1639,11 @@ b200lu_status b200lu_batch_solve_refine_staged(b200lu_batch* h, int refine, cons
     h->last_error = "max_iterations exceeds the handle's refine_capacity";
     return B200LU_INVALID_ARGUMENT;
   }
-  const int buf = h->stage_cur;
+  const int buf = h->rhs_queue.front();
+  h->rhs_queue.erase(h->rhs_queue.begin());
   CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_in[buf], 0));
   ST_TRY(to_interleaved(h, h->n, h->d_stage_rhs[buf], h->d_b));
   CU_TRY(h, cudaEventRecord(h->ev_rhs_used[buf], h->stream));
-  h->staged_rhs = false;
   ST_TRY(solve_int(h, h->d_b, h->d_x));
   b200lu_status fail = collect_upper_failure(h, failed_rows);
   const double* result = h->d_x;

@@ -85,6 +85,39 @@ class SolveReport:
                           "systems_solved": self.systems_solved, "reanalysis_count": self.reanalysis_count}}, indent=2)
 
 
+    def to_csv(self) -> str:  # report_to_csv, src/report.cpp:100-119: same header, %.17g numbers, '#' trailer
+        def g(x):
+            return f"{x:.17g}"
+        out = ["k,n,nnz,analyze_ms,scatter_ms,factor_ms,trisolve_ms,refine_ms,refine_iters,relres_direct,relres_final,status"]
+        for r in self.systems:
+            out.append(",".join([str(r.k), str(r.n), str(r.nnz), g(r.analyze_ms), g(r.scatter_ms), g(r.factor_ms),
+                                 g(r.trisolve_ms), g(r.refine_ms), str(r.refine_iters), g(r.relres_direct),
+                                 g(r.relres_final), r.status]))
+        out.append("# total_ms," + g(self.total_ms))
+        for name in ("analyze", "scatter", "factor", "trisolve", "refine"):
+            out.append(f"# mean_{name}_ms," + g(getattr(self, f"mean_{name}_ms")))
+        out.append(f"# systems_solved,{self.systems_solved}")
+        out.append(f"# reanalysis_count,{self.reanalysis_count}")
+        return "\n".join(out) + "\n"
+
+    @staticmethod
+    def from_json(text: str) -> "SolveReport":  # report_from_json, src/report.cpp:68-98
+        try:
+            d = json.loads(text)
+            rep = SolveReport()
+            for jr in d["systems"]:
+                rep.systems.append(SystemRecord(**{k: jr[k] for k in SystemRecord.__dataclass_fields__}))
+            agg = d["aggregate"]
+            rep.total_ms = float(agg["total_ms"])
+            for name in ("analyze", "scatter", "factor", "trisolve", "refine"):
+                setattr(rep, f"mean_{name}_ms", float(agg["mean_phase_ms"][name]))
+            rep.systems_solved = int(agg["systems_solved"])
+            rep.reanalysis_count = int(agg["reanalysis_count"])
+            return rep
+        except (KeyError, TypeError, ValueError) as e:
+            raise rlu.Error(f"malformed report: {e}")
+
+
 @dataclass
 class KktSystem:
     """rlu::KktSystem (include/rlu/kkt.hpp:23-28)."""

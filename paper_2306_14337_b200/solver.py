@@ -428,6 +428,32 @@ def classic_refine(f: NumericFactors, b, x0, config: RefineConfig | None = None,
     return _refine("b200lu_refine_classic", f, b, x0, config, preconditioned)
 
 
+@dataclass
+class Cgs2Result:
+    """include/rlu/refine.hpp:25-30."""
+    coefficients: np.ndarray
+    vector: np.ndarray
+    norm: float
+    breakdown: bool
+
+
+def cgs2_orthonormalize(f: NumericFactors, basis, v) -> Cgs2Result:
+    """cgs2_orthonormalize, src/refine.cpp:8-26, on the device of handle `f` (vectors of length f.symbolic.n):
+    two full Gram-Schmidt passes of v against the orthonormal rows of `basis` ([k, n]), then normalisation."""
+    n = f.symbolic.n
+    B = np.ascontiguousarray(basis, dtype=np.float64).reshape(-1, n) if np.size(basis) else np.zeros((0, n))
+    vv = _f64(v)
+    if vv.size != n:
+        raise DimensionError(f"cgs2_orthonormalize: vector length {vv.size}, expected {n}")
+    k = B.shape[0]
+    coef = np.zeros(max(k, 1), dtype=np.float64)
+    out = np.empty(n, dtype=np.float64)
+    norm, bd = C.c_double(), C.c_int()
+    f._check(_capi.lib().b200lu_cgs2_orthonormalize(f._h, k, B.ctypes.data, vv.ctypes.data, 0, coef.ctypes.data,
+                                                    out.ctypes.data, C.byref(norm), C.byref(bd)))
+    return Cgs2Result(coef[:k], out, float(norm.value), bool(bd.value))
+
+
 def kkt_bind(f: NumericFactors, n_primal: int, h_diag, diag_source_pos):
     """Prepares the device-resident KKT value path (include/b200lu.h, b200lu_kkt_bind): H's own
     diagonal and the position of every K_ii in source-CSR order."""

@@ -338,3 +338,42 @@ def test_pattern_the_tiled_kernel_cannot_take_keeps_the_row_blocked_one(tiles_en
             assert np.array_equal(f.values(s), fx.oracle.factorize(vals[s])[0])
     finally:
         f.close()
+
+
+def test_staged_pipeline_matches_the_plain_calls_bitwise():
+    """The staged (pipelined) submission — inputs of batch k + 1 copied while batch k is processed, solutions
+    leaving on their own stream — gives, for every batch of a sequence, exactly the results of the plain
+    refactorize / solve_system / fgmres_refine calls."""
+    import torch
+    fx = golden_fixture("kkt_small")
+    batch, steps = 5, 4
+    seq = []
+    for k in range(steps):
+        vals, rhs = _scenarios(fx, batch)
+        seq.append((torch.from_numpy(vals * (1.0 + 0.125 * k)).pin_memory(), torch.from_numpy(rhs * (1.0 - 0.25 * k)).pin_memory()))
+    f = BatchedFactors(fx.sym, batch)
+    g = BatchedFactors(fx.sym, batch)
+    try:
+        outs = [torch.empty((batch, fx.n), dtype=torch.float64).pin_memory() for _ in range(steps)]
+        f.stage_inputs(seq[0][0], seq[0][1])
+        iters = []
+        for k in range(steps):
+            if k + 1 < steps:
+                f.stage_inputs(seq[k + 1][0], seq[k + 1][1])
+                if k == 0:
+                    with pytest.raises(rlu.Error):  # both staging sets hold unconsumed inputs
+                        f.stage_inputs(seq[k + 1][0], seq[k + 1][1])
+            f.refactorize_staged()
+            iters.append([o.iterations for o in f.solve_refine_staged(outs[k])])
+        f.staged_wait()
+        for k in range(steps):
+            g.refactorize(seq[k][0].numpy())
+            x = g.solve_system(seq[k][1].numpy())
+            xr, ocs = g.fgmres_refine(seq[k][1].numpy(), x)
+            assert np.array_equal(outs[k].numpy(), xr), k
+            assert iters[k] == [o.iterations for o in ocs]
+        with pytest.raises(rlu.Error):
+            f.refactorize_staged()  # nothing staged any more
+    finally:
+        f.close()
+        g.close()

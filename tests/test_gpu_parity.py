@@ -500,3 +500,59 @@ def test_scenario_batch_matches_single_handle_runs():
         assert records[s].scenario == s and records[s].failed_row == -1
         assert records[s].refine_iters == out.iterations and records[s].relres_final <= 1e-14
     batch.close()
+
+
+# ---------------------------------------------------------------- cgs2_orthonormalize at the boundary
+# proj/tests/test_refine.cpp:34-79 restated against b200lu_cgs2_orthonormalize.
+
+def _identity_handle(n):
+    fx = dense_fixture(np.eye(n))
+    return rlu.NumericFactors(fx.sym)
+
+
+def _unit(n, i):
+    e = np.zeros(n)
+    e[i] = 1.0
+    return e
+
+
+@needs_ref
+def test_cgs2_exact_cases():
+    f = _identity_handle(3)
+    try:
+        r = rlu.cgs2_orthonormalize(f, [_unit(3, 0)], _unit(3, 1))    # already orthogonal: left alone
+        assert not r.breakdown and r.coefficients[0] == 0.0 and np.array_equal(r.vector, _unit(3, 1)) and r.norm == 1.0
+        r = rlu.cgs2_orthonormalize(f, [_unit(3, 0)], _unit(3, 0) + _unit(3, 1))  # projects exactly
+        assert not r.breakdown and r.coefficients[0] == 1.0 and np.array_equal(r.vector, _unit(3, 1))
+        r = rlu.cgs2_orthonormalize(f, [_unit(3, 0)], _unit(3, 0))    # happy breakdown on subspace membership
+        assert r.breakdown
+        r = rlu.cgs2_orthonormalize(f, np.zeros((0, 3)), np.array([3.0, 0.0, 4.0]))  # empty basis: plain normalisation
+        assert not r.breakdown and r.norm == 5.0 and np.array_equal(r.vector, np.array([0.6, 0.0, 0.8]))
+        with pytest.raises(rlu.DimensionError):
+            rlu.cgs2_orthonormalize(f, [_unit(3, 0)], np.ones(4))
+    finally:
+        f.close()
+
+
+@needs_ref
+def test_cgs2_restores_orthogonality_lost_by_a_single_pass():
+    n = 50
+    f = _identity_handle(n)
+    rng = rb.RefRng(71)
+    basis = []
+    try:
+        for k in range(20):
+            v = rng.random_vector(n)
+            if basis:  # nearly dependent on the basis: stresses the re-orthogonalisation pass
+                v = basis[0] + 1e-9 * v
+            r = rlu.cgs2_orthonormalize(f, np.array(basis), v)
+            assert not r.breakdown
+            for q in basis:
+                assert abs(ob.dot(q, r.vector)) <= 1e-13
+            # against the reference itself: same coefficients and vector up to the rounding of the dot products
+            cref, vref, nref, bref = rb.cgs2(np.array(basis), v)
+            assert not bref and nref == pytest.approx(r.norm, rel=1e-12)
+            assert np.allclose(r.coefficients, cref, rtol=1e-12, atol=1e-15)
+            basis.append(r.vector)
+    finally:
+        f.close()
