@@ -376,6 +376,9 @@ typedef struct {
 b200lu_status b200lu_tile_plan_emulate(const b200lu_symbolic_view* sym, int rows_per_tile, int64_t tile_entries,
                                        int64_t tail_width, double pivot_floor, double* values, int64_t* failed_row,
                                        b200lu_tile_plan_stats* stats, char* error_buf, int error_buf_len);
+/* Diagnostics: the 16 phase counters (clock cycles summed over warps) of the tiled refactorization kernel;
+ * all zero unless the library was built with -DB200LU_TILE_PROF (csrc/tile.cuh lists the phases). */
+b200lu_status b200lu_batch_tile_profile(b200lu_batch* h, int64_t* cycles_out, int reset);
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled);
 b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset);
 b200lu_status b200lu_batch_synchronize(b200lu_batch* h);

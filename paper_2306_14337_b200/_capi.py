@@ -117,6 +117,7 @@ EXPORTS = {
     "b200lu_batch_get_info": (i32, [vp, C.POINTER(BatchInfo)]),
     "b200lu_tile_plan_emulate": (i32, [C.POINTER(SymbolicView), i32, i64, i64, dbl, vp, C.POINTER(i64),
                                        C.POINTER(TilePlanStats), C.c_char_p, i32]),
+    "b200lu_batch_tile_profile": (i32, [vp, vp, i32]),
     "b200lu_batch_set_timing": (i32, [vp, i32]),
     "b200lu_batch_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
     "b200lu_batch_synchronize": (i32, [vp]),

@@ -76,7 +76,8 @@ struct b200lu_batch {
   int block_grid = 0;
   size_t block_smem = 0;
   // tiled trailing part (tile.cuh): rows resident in shared memory, pivot rows streamed by TMA
-  bool use_tiles = false;
+  bool use_tiles = false, tile_auto = true;
+
   std::string tile_note;          // why the tiled kernel is not used, if it is not
   TileMeta* d_tile_meta = nullptr;
   TileRow* d_tile_rows = nullptr;
@@ -84,6 +85,7 @@ struct b200lu_batch {
   RowItem* d_tile_row_items = nullptr;
   uint16_t* d_tile_dest = nullptr;
   int32_t* d_tile_flags = nullptr;  // [n][tile_units]
+  long long* d_tile_prof = nullptr; // phase counters of the tiled kernel (-DB200LU_TILE_PROF builds)
   int32_t n_tiles = 0, tile_units = 0, tile_rows_per = 8, tile_ring_blocks = 32, tile_ctas = 2;
   int64_t tile_fetched_entries = 0;
   void (*tile_fn)(BTileArgs) = nullptr;
@@ -344,6 +346,8 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
     if (h->n_blocks > 0) {
       BBlockArgs bb;
       bb.n_blocks = h->n_blocks;
+      bb.first_unit = 0;
+      bb.units_here = h->units;
       bb.units = h->units;
       bb.gen = h->gen;
       bb.blocks = h->d_blocks;
@@ -820,7 +824,16 @@ b200lu_status setup_tiles(H* h, const std::vector<int32_t>& tail_rows) {
   for (int32_t i : tail_rows) max_row = std::max<int64_t>(max_row, S.row_ptr[i + 1] - S.row_ptr[i] + kTileSpare);  // + the spare entries
   const int64_t row_bytes = static_cast<int64_t>(kTileScen * sizeof(double));
   int64_t budget = std::min(max_block, sm_bytes / ctas - 1024) - overhead;  // 1 KB per CTA is reserved by the driver
-  if (max_row * row_bytes > budget) budget = max_block - overhead;
+  if (max_row * row_bytes > budget) {
+    // The longest row needs more than a CTA's share of the SM: one CTA per SM. That halves the tiles in
+    // flight and measured slower than the row-blocked kernel (C3, longest row 1 951 entries = 125 KB:
+    // 27.0 ms against 23.1 ms at 32 scenarios, 46.9 against 33.7 at 64): only when asked for.
+    if (h->tile_auto) {
+      h->tile_note = "the longest trailing row (" + std::to_string(max_row) + " entries) leaves room for one tile CTA per SM only";
+      return B200LU_OK;
+    }
+    budget = max_block - overhead;
+  }
   if (budget < max_row * row_bytes) {
     h->tile_note = "a trailing row of " + std::to_string(max_row) + " entries does not fit a tile";
     return B200LU_OK;
@@ -893,6 +906,9 @@ b200lu_status finish_tiles(H* h, int sm_count) {
   ta.pivot_floor = h->pivot_floor;
   ta.failed = h->d_failed;
   ta.ticket = h->d_tickets + 1;
+  ST_TRY(dev_alloc(h, &h->d_tile_prof, 16));
+  CU_TRY(h, cudaMemsetAsync(h->d_tile_prof, 0, 16 * sizeof(long long), h->stream));
+  ta.prof = h->d_tile_prof;
   const int variant = h->tile_rows_per == 16 ? 1 : h->tile_ctas == 3 ? 2 : 0;
   h->tile_fn = variant == 1 ? bfactor_tile_kernel<16, 32, 2> : variant == 2 ? bfactor_tile_kernel<8, 16, 3> : bfactor_tile_kernel<8, 32, 2>;
   // per function, process-wide: never lowered under a live handle (the largest request so far stays)
@@ -1031,11 +1047,16 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     //   * bfactor_block_kernel (batch.cuh): 2-row blocks x 32 scenarios, updates as L2 reductions: the faster
     //     one once the batch is THROUGHPUT-bound.
     // B200LU_BATCH_TILES = 1 / 0 forces one of them; default: tiles up to 96 scenarios per handle (an 8-GPU
-    // shard of the 256-scenario batch is 32). A pattern / batch the tiled kernel cannot take (a row larger than
+    // shard of the 256-scenario batch is 32), provided two tile CTAs fit on an SM (setup_tiles). A pattern / batch the tiled kernel cannot take (a row larger than
     // a tile, a pivot row longer than a staging copy, more than 2^31 entries per tensor-map dimension) keeps
     // the row-blocked kernel.
     e = std::getenv("B200LU_BATCH_TILES");
-    const bool want_tiles = e ? std::atoi(e) != 0 : h->padded <= 96;
+    const bool forced = e != nullptr;
+    const bool want_tiles = forced ? std::atoi(e) != 0 : h->padded <= 96;
+    h->tile_auto = !forced;
+    // (Running both side by side — the tiled kernel on some of the scenarios, the row-blocked one on the rest, one
+    // CTA of each per SM on two streams — was measured at C2 x 256: 35-46 ms against 24.4 ms for the row-blocked
+    // kernel alone; dropped.)
     if (want_tiles && !tail_rows.empty() && tail_mode != 0) {
       ST_TRY(setup_tiles(h, tail_rows));
       if (h->use_tiles) {
@@ -1296,7 +1317,7 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_tile_prof, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
                   h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
@@ -1765,6 +1786,18 @@ b200lu_status b200lu_tile_plan_emulate(const b200lu_symbolic_view* sym, int rows
     stats->consumed_entries = consumed;
   }
   return failed >= 0 ? B200LU_ZERO_PIVOT : B200LU_OK;
+}
+
+b200lu_status b200lu_batch_tile_profile(b200lu_batch* h, int64_t* cycles_out, int reset) {
+  if (!h || !cycles_out) return B200LU_INVALID_ARGUMENT;
+  for (int i = 0; i < 16; ++i) cycles_out[i] = 0;
+  if (!h->d_tile_prof) return B200LU_OK;
+  CU_TRY(h, cudaSetDevice(h->device));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  static_assert(sizeof(long long) == sizeof(int64_t), "counter width");
+  CU_TRY(h, cudaMemcpy(cycles_out, h->d_tile_prof, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (reset) CU_TRY(h, cudaMemset(h->d_tile_prof, 0, 16 * sizeof(int64_t)));
+  return B200LU_OK;
 }
 
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled) {

@@ -388,7 +388,8 @@ struct MergedPivot {
 
 struct BBlockArgs {
   int32_t n_blocks;
-  int32_t units;
+  int32_t first_unit, units_here;  // this launch handles units [first_unit, first_unit + units_here) of every block
+  int32_t units;                   // units per row (stride of the flag array)
   int32_t gen;
   const BlockMeta* blocks;
   const MergedPivot* merged;
@@ -442,14 +443,14 @@ bfactor_block_kernel(const BBlockArgs a) {
   double* stage = block_smem + static_cast<size_t>(threadIdx.x >> 5) * block_stage_doubles();
   static_assert(kBlockStage == 0 || S == 32, "staging assumes one lane per scenario");
   static_assert(kBlockStage * sizeof(DestT) + 8 <= kBlockStageDest * sizeof(double), "destination slice does not fit");
-  const unsigned long long total = static_cast<unsigned long long>(a.n_blocks) * a.units;
+  const unsigned long long total = static_cast<unsigned long long>(a.n_blocks) * a.units_here;
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(a.ticket, 1ull);
     t = __shfl_sync(full, t, 0);
     if (t >= total) break;
-    const int32_t b = static_cast<int32_t>(t / a.units);
-    const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units);
+    const int32_t b = static_cast<int32_t>(t / a.units_here);
+    const int32_t u = a.first_unit + static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units_here);
     const int4 b0 = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
     const int4 b1 = __ldg(reinterpret_cast<const int4*>(a.blocks + b) + 1);
     const int32_t rows4[4] = {b0.x, b0.y, b0.z, b0.w};

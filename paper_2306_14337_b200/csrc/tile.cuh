@@ -37,6 +37,31 @@
 #define B200LU_TILE_SPIN_NS 32
 #endif
 
+// Optional phase accounting (-DB200LU_TILE_PROF): every warp adds the clock cycles it spends in each phase of
+// the tiled kernel to BTileArgs::prof[phase] (16 counters), read back by tools/tile_prof.py.
+#ifdef B200LU_TILE_PROF
+#define TPROF_DECL long long tprof_t = clock64(); long long tprof_acc[16] = {0}
+#define TPROF(ph)                                  \
+  do {                                             \
+    const long long tprof_n = clock64();           \
+    tprof_acc[ph] += tprof_n - tprof_t;            \
+    tprof_t = tprof_n;                             \
+  } while (0)
+#define TPROF_FLUSH(a)                                                                                  \
+  do {                                                                                                  \
+    if ((threadIdx.x & 31) == 0) {                                                                      \
+      for (int tprof_i = 0; tprof_i < 16; ++tprof_i) {                                                  \
+        if (tprof_acc[tprof_i]) atomicAdd(reinterpret_cast<unsigned long long*>((a).prof) + tprof_i,    \
+                                          static_cast<unsigned long long>(tprof_acc[tprof_i]));         \
+      }                                                                                                 \
+    }                                                                                                   \
+  } while (0)
+#else
+#define TPROF_DECL
+#define TPROF(ph)
+#define TPROF_FLUSH(a)
+#endif
+
 namespace b200lu {
 
 constexpr int kTileCtlBytes = 1280;
@@ -60,6 +85,7 @@ struct BTileArgs {
   double pivot_floor;
   int32_t* failed;
   unsigned long long* ticket;
+  long long* prof;              // 16 phase counters (cycles summed over warps), only with -DB200LU_TILE_PROF
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -146,12 +172,18 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
   }
   int32_t ext_base = 0;  // copies issued for the tiles this CTA has already processed
   const unsigned long long total = static_cast<unsigned long long>(a.n_tiles) * a.units;
+  TPROF_DECL;
   while (true) {
     __syncthreads();  // the previous tile is finished: its shared memory may be reused
+    TPROF(0);
+    // (Claiming the next ticket one tile ahead, to hide the atomic's round trip, measured 46 ms against 27.6:
+    // a held ticket delays its dependents for a whole tile.)
     if (threadIdx.x == 0) *s_ticket = atomicAdd(a.ticket, 1ull);
     if (threadIdx.x < R) done[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long t = *s_ticket;
+    TPROF(1);  // end of the previous tile (BAR.SYNC blocks at its first dependent instruction: the waiting for the
+               // slowest row and the idle warps of short tiles show up here, not under phase 0) + the claim
     if (t >= total) break;
     const int32_t b = static_cast<int32_t>(t / a.units);
     const int32_t u = static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units);
@@ -167,7 +199,11 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
       // parallel; lane 0 then issues the copies in order: ring space (the oldest copies are retired once
       // all their consumers have released them), the flag if the probe found it unset, one TMA copy.
       int32_t head = 0, used = 0, oldest = 0;  // lane 0: ring allocator state of this tile
+#ifdef B200LU_EXP_NO_SYNC  // timing experiment: no producer at all
+      for (int32_t b0 = 0; b0 < 0; b0 += 32) {
+#else
       for (int32_t b0 = 0; b0 < n_ext; b0 += 32) {
+#endif
         if (b0 + lane < n_ext) {
           const int4 my = __ldg(reinterpret_cast<const int4*>(a.ext + ext_beg + b0 + lane));
           int32_t ready = 1;
@@ -189,6 +225,7 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
             const int nb = (static_cast<int>(cf & 0xffu) + kTileBoxStep - 1) / kTileBoxStep;  // 1..kTileMaps blocks
             const int start = static_cast<int>(cf >> 24);  // ring positions are static (tile_plan.hpp); only the space is awaited
             const int waste = start < head ? RB - head : 0;  // the planner wrapped: the blocks left at the end are skipped
+            TPROF(10);  // producer: bookkeeping
             while (x - oldest >= kTileSlots || used + nb + waste > RB) {
               const int os = (ext_base + oldest) & (kTileSlots - 1);
               while (*reinterpret_cast<volatile int32_t*>(released + os) != p_expect[os]) {
@@ -196,6 +233,7 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
               used -= p_blocks[os];
               ++oldest;
             }
+            TPROF(11);  // producer: waiting for ring space (the consumers)
             head = start + nb;
             used += nb + waste;
             *reinterpret_cast<volatile int32_t*>(released + slot) = 0;
@@ -206,6 +244,7 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
             // It does not have to wait for the copy itself: a consumer that comes early sleeps on the mbarrier.
             __threadfence_block();
             *issued = gx + 1;
+            TPROF(10);
             if (!p_ready[q]) {
               const int32_t* f = a.flags + static_cast<int64_t>(d) * a.units + u;
               unsigned ns = 32;
@@ -214,21 +253,30 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
                 ns = min(ns * 2, 256u);
               }
             }
+            TPROF(12);  // producer: waiting for a pivot row of another tile
             // The flag is read with a RELAXED gpu-scope load and followed by a generic->async proxy fence,
             // not by an acquire: the only reader of the data the flag guards is the TMA engine (async proxy,
             // served by L2, where the owner's fenced stores already are when the flag is visible); no thread of
             // this kernel reads a pivot row of another tile through the generic proxy, so the L1 invalidation
             // that ld.acquire.gpu costs (LDG.STRONG + CCTL.IVALL, measured: the top stall of this warp) would
             // protect nothing.
-            asm volatile("fence.proxy.async.global;" ::: "memory");
+            // Only a pivot row finished by THIS launch needs the fence (the rows of the head launch and of the
+            // scatter pass crossed a kernel boundary).
+            if ((cf >> 16) & kItemWait) asm volatile("fence.proxy.async.global;" ::: "memory");
+#ifdef B200LU_EXP_NO_TMA  // timing experiment: no copy, the consumers read whatever is in the ring
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+#else
             mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(nb * kTileBlockDoubles * sizeof(double)));
             tma_load_2d(ring + static_cast<size_t>(start) * kTileBlockDoubles, &a.maps[nb - 1], (u & 3) * kTileScen,
                         static_cast<int32_t>(group_base + entry), full + slot);
+#endif
+            TPROF(13);  // producer: fence + copy issue
           }
         }
         __syncwarp();
       }
     } else if (warp < nrows) {
+      TPROF(15);
       // ------------------------------------------------------------ consumer: one row of the tile
       const int4 r0 = __ldg(reinterpret_cast<const int4*>(a.rows + row_beg + warp));
       const int4 r1 = __ldg(reinterpret_cast<const int4*>(a.rows + row_beg + warp) + 1);
@@ -245,6 +293,7 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
       *reinterpret_cast<double2*>(myrow2 + static_cast<size_t>(len + e) * kTileScen) = make_double2(0.0, 0.0);  // this lane's spare entry
       cp_async_commit_wait_all();
       __syncwarp();
+      TPROF(2);  // row load
 
       const uint32_t ring_a = smem_u32(ring), rows_a = smem_u32(rowsm), my2_a = smem_u32(myrow2);
       const uint32_t issued_a = smem_u32(const_cast<int32_t*>(issued));
@@ -271,19 +320,27 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
           const bool internal = (fl & kItemInternal) != 0;
           uint32_t src_a;
           int slot = 0;
+          TPROF(3);  // item records, shuffles, destination prefetch
           if (internal) {
+#ifndef B200LU_EXP_NO_SYNC
             while (lds32_volatile(done_a + 4 * srcid) == 0) {
               if (B200LU_TILE_SPIN_NS) __nanosleep(B200LU_TILE_SPIN_NS);
             }
+#endif
             __threadfence_block();
             src_a = rows_a + static_cast<uint32_t>(lds32_volatile(uoff_a + 4 * srcid)) * (kTileScen * 8);
+            TPROF(4);  // waiting for a row of this tile
           } else {
             const int32_t gx = ext_base + srcid;
             slot = gx & (kTileSlots - 1);
+#ifndef B200LU_EXP_NO_SYNC
             while (lds32_volatile(issued_a) <= gx) {
               if (B200LU_TILE_SPIN_NS) __nanosleep(B200LU_TILE_SPIN_NS);
             }
+            TPROF(5);  // waiting for the producer to reach the item
             mbar_wait(full + slot, static_cast<uint32_t>(gx / kTileSlots) & 1u);
+            TPROF(6);  // waiting for the copy to land
+#endif
             src_a = ring_a + ((fl >> 8) & 0xffu) * (kTileBlockDoubles * 8);
           }
           uint32_t sl_a = src_a + e * (kTileScen * 8) + sp * 16;
@@ -295,7 +352,12 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
             sl_a += kTileScen * 8;  // the diagonal is entry 0 of a first chunk
             --cnt;
           }
+          TPROF(7);  // alpha
+#ifdef B200LU_EXP_NO_UPDATES  // timing experiment: waits, alpha and release only
+          const int32_t iters = 0;
+#else
           const int32_t iters = (cnt + kTileIter - 1) / kTileIter;
+#endif
           for (int32_t g0 = 0; g0 < iters; g0 += kTileGroup) {
             const uint32_t ww[4] = {wd.x, wd.y, wd.z, wd.w};
             if (g0 + kTileGroup < iters) wd = __ldg(tw + static_cast<size_t>(g0 / kTileGroup + 1) * kTileEntryLanes);
@@ -332,14 +394,18 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
               }
             }
           }
+          TPROF(8);  // updates
           __syncwarp();  // every lane's updates are in shared memory before the next pivot reads them
+#ifndef B200LU_EXP_NO_SYNC
           if (!internal && lane == 0) atomicAdd(released + slot, 1);
+#endif
           if (fl & kItemLast) {
             if (e == 0) sts128(my2_a + k * (kTileScen * 8), alpha);  // l_id, src/numeric.cpp:41
             ++k;
           }
         }
       }
+      TPROF(3);
       // ---- the row is final. Order: (1) intra-tile hand-off, (2) pivot check, (3) diagonal + upper part to
       // global memory and the ready flag (what other tiles wait for), (4) the lower part.
       __syncwarp();
@@ -363,9 +429,11 @@ bfactor_tile_kernel(const __grid_constant__ BTileArgs a) {
         const double2 v = *reinterpret_cast<const double2*>(myrow + static_cast<size_t>(j) * kTileScen + (lane & 3) * 2);
         __stcg(reinterpret_cast<double2*>(grow + static_cast<int64_t>(j) * 32 + (lane & 3) * 2), v);
       }
+      TPROF(9);  // publication + write-back
     }
     ext_base += n_ext;
   }
+  TPROF_FLUSH(a);
 }
 
 }  // namespace b200lu
