@@ -1351,8 +1351,8 @@ b200lu_status b200lu_batch_check_pattern(const b200lu_batch* h, int64_t n, const
                                          const int64_t* col_indices) {
   if (!h || !row_offsets || (!col_indices && h->nnz_source)) return B200LU_INVALID_ARGUMENT;
   if (n != h->n) return B200LU_PATTERN_MISMATCH;
-  if (std::memcmp(row_offsets, h->src_row_offsets.data(), sizeof(int64_t) * (n + 1)) != 0) return B200LU_PATTERN_MISMATCH;
-  if (h->nnz_source && std::memcmp(col_indices, h->src_col_indices.data(), sizeof(int64_t) * h->nnz_source) != 0) {
+  if (!same_bytes(row_offsets, h->src_row_offsets.data(), sizeof(int64_t) * (n + 1))) return B200LU_PATTERN_MISMATCH;
+  if (h->nnz_source && !same_bytes(col_indices, h->src_col_indices.data(), sizeof(int64_t) * h->nnz_source)) {
     return B200LU_PATTERN_MISMATCH;
   }
   return B200LU_OK;

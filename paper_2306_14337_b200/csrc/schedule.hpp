@@ -8,13 +8,95 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "b200lu.h"
 
 namespace b200lu {
+
+// pattern_equal's comparison (src/numeric.cpp:15, src/sparse.cpp) runs on EVERY scatter, as in the reference; at
+// n = 1.6 M that is 85 MB of indices per call — 8 ms single-threaded, a third of the whole device step — so large
+// comparisons are split over a few persistent host threads (created on first use, parked on a condition variable
+// between calls: dispatch costs tens of microseconds, not a thread spawn per call).
+class CompareBytesPool {
+ public:
+  static CompareBytesPool& instance() {
+    static CompareBytesPool pool;
+    return pool;
+  }
+  bool same(const void* a, const void* b, size_t bytes) {
+    constexpr size_t kChunk = size_t{1} << 20;
+    const size_t parts = std::min<size_t>(workers_.size() + 1, bytes / kChunk);
+    if (parts < 2) return std::memcmp(a, b, bytes) == 0;
+    std::lock_guard<std::mutex> call_lock(call_);  // one comparison at a time
+    const size_t step = (bytes + parts - 1) / parts;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      a_ = static_cast<const char*>(a);
+      b_ = static_cast<const char*>(b);
+      bytes_ = bytes;
+      step_ = step;
+      parts_ = parts;
+      pending_ = parts - 1;
+      differ_ = false;
+      ++generation_;
+    }
+    cv_.notify_all();
+    if (std::memcmp(a_, b_, std::min(step, bytes)) != 0) differ_ = true;  // part 0 on the calling thread
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    return !differ_;
+  }
+
+ private:
+  CompareBytesPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const unsigned n = std::min(7u, hw - 1);
+    for (unsigned t = 0; t < n; ++t) workers_.emplace_back([this, t] { run(t + 1); });
+  }
+  ~CompareBytesPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+      ++generation_;
+    }
+    cv_.notify_all();
+    for (std::thread& th : workers_) th.join();
+  }
+  void run(size_t part) {
+    uint64_t seen = 0;
+    while (true) {
+      std::unique_lock<std::mutex> lk(m_);
+      cv_.wait(lk, [&] { return generation_ != seen; });
+      seen = generation_;
+      if (stop_) return;
+      if (part >= parts_) continue;
+      const char *a = a_, *b = b_;
+      const size_t lo = part * step_, hi = std::min(bytes_, lo + step_);
+      lk.unlock();
+      const bool diff = lo < hi && std::memcmp(a + lo, b + lo, hi - lo) != 0;
+      lk.lock();
+      if (diff) differ_ = true;
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_, call_;
+  std::condition_variable cv_, done_;
+  const char *a_ = nullptr, *b_ = nullptr;
+  size_t bytes_ = 0, step_ = 0, parts_ = 0, pending_ = 0;
+  uint64_t generation_ = 0;
+  std::atomic<bool> differ_{false};
+  bool stop_ = false;
+};
+inline bool same_bytes(const void* a, const void* b, size_t bytes) { return CompareBytesPool::instance().same(a, b, bytes); }
 
 // One record per claim position, so a worker learns everything about its row from one 16-byte
 // load instead of a chain of dependent index loads.

@@ -87,3 +87,27 @@ def test_batch_bitwise_at_c2():
     # the reference's own residual of the same solution agrees (checker: the reference's relative_residual)
     assert seqs[5].matrix(0).relative_residual(xr[5], rhs[5]) <= 1e-14
     f.close()
+
+
+def test_pattern_guard_at_full_size_sees_a_change_in_any_chunk():
+    """pattern_equal (src/numeric.cpp:15-17) runs on every scatter; above 2 MB the comparison is split over host
+    threads: a single changed index anywhere — first row offset, last column index — must still be refused."""
+    fx = kkt_fixture(*C2, num_systems=1)
+    f = rlu.NumericFactors(fx.sym)
+    try:
+        rlu.refactorize(f, fx.matrix(0))
+        for where in (1, len(fx.ci) // 2, len(fx.ci) - 1):
+            ci = fx.ci.copy()
+            ci[where] = ci[where] + 1 if where == len(ci) - 1 or ci[where] + 1 != ci[where + 1] else ci[where] - 1
+            with pytest.raises(rlu.PatternMismatchError):
+                rlu.refactorize(f, rlu.CsrMatrix(fx.n, fx.n, fx.ro, ci, fx.values[0]))
+        ro = fx.ro.copy()
+        ro[len(ro) // 2] += 1
+        with pytest.raises(rlu.PatternMismatchError):
+            rlu.refactorize(f, rlu.CsrMatrix(fx.n, fx.n, ro, fx.ci, fx.values[0]))
+        with pytest.raises(rlu.PatternMismatchError):  # a value array of the wrong length
+            rlu.refactorize(f, rlu.CsrMatrix(fx.n, fx.n, fx.ro, fx.ci, fx.values[0][:-1]))
+        rlu.refactorize(f, fx.matrix(0))  # and the handle still works
+        assert np.array_equal(f.values, fx.oracle.factorize(fx.values[0])[0])
+    finally:
+        f.close()

@@ -6,7 +6,8 @@ import collections, csv, json, os, shutil, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
-WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+WANT = ["gpu__time_duration.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
@@ -88,7 +89,7 @@ def main():
     traffic = {}
     seen = set()
     for rep in reps:
-        for kr in ("factor_kernel", "factor_block_kernel", "tri_kernel", "tail_kernel"):
+        for kr in ("factor_kernel", "factor_block_kernel", "factor_tile_kernel", "tri_kernel", "tail_kernel"):
             ms = raw_metrics(rep, kr)
             if not ms:
                 continue
@@ -98,7 +99,7 @@ def main():
                 for w in WANT:
                     if w in m:
                         md.append(f"  * {w} = {m[w][0]} {m[w][1]}")
-                if kr in ("factor_kernel", "factor_block_kernel") and "dram__bytes_read.sum" in m and kr not in seen:
+                if kr in ("factor_kernel", "factor_block_kernel", "factor_tile_kernel") and "dram__bytes_read.sum" in m and kr not in seen:
                     # one refactorization = the head launch + the row-blocked trailing launch: their traffic adds up
                     seen.add(kr)
                     def mb(x):
