@@ -283,7 +283,7 @@ def _guard_pattern(f: NumericFactors, A: CsrMatrix):
         st = _capi.lib().b200lu_check_pattern(f._h, A.nrows, ro.ctypes.data, ci.ctypes.data)
     if st != _capi.OK:
         raise PatternMismatchError("matrix pattern differs from the analyzed pattern")
-    if not A.has_values():
+    if A.values is None:
         raise Error("scatter_values: matrix has no values")
     nvals = A.values.numel() if _is_device_tensor(A.values) else np.asarray(A.values).size
     if nvals != ci.size:
