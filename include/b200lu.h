@@ -44,7 +44,9 @@ typedef enum {
   B200LU_INVALID_FACTORS = 4,  /* rlu::Error("...: factors are not valid"), src/trisolve.cpp:20 */
   B200LU_CUDA_ERROR = 5,
   B200LU_INVALID_ARGUMENT = 6,
-  B200LU_NO_DEVICE = 7
+  B200LU_NO_DEVICE = 7,
+  B200LU_ZERO_DIAGONAL = 8,         /* rlu::ZeroDiagonalError{row}, host analysis (src/symbolic.cpp:121-123) */
+  B200LU_STRUCTURALLY_SINGULAR = 9  /* rlu::StructurallySingularError{deficient_rows}, host analysis (src/matching.cpp:27-31,49-52,132-143) */
 } b200lu_status;
 
 /* Borrowed, read-only image of rlu::SymbolicFactors
@@ -382,6 +384,32 @@ b200lu_status b200lu_batch_tile_profile(b200lu_batch* h, int64_t* cycles_out, in
 b200lu_status b200lu_batch_set_timing(b200lu_batch* h, int enabled);
 b200lu_status b200lu_batch_get_phase_times(b200lu_batch* h, double* ms_out, int64_t* count_out, int reset);
 b200lu_status b200lu_batch_synchronize(b200lu_batch* h);
+
+/* ---- Host-side symbolic analysis --------------------------------------------------------
+ * rlu::symbolic_analyze(A, AnalyzeOptions{use_scaling, use_amd}) (include/rlu/symbolic.hpp:67-75,
+ * src/symbolic.cpp:156-203) with mc64_scale (src/matching.cpp:17-189), amd_order (src/ordering.cpp:9-122) and
+ * fill1_pattern (src/symbolic.cpp:95-154): the same permutations, scale factors, combined L+U pattern, diag_pos
+ * and scatter map BIT FOR BIT, from algorithms whose cost follows the size of the result (csrc/analyze.cpp).
+ * Host code only: no device is needed or used. `values` (nnz doubles, source order) is read only when
+ * use_scaling != 0. On every return with *out != NULL the object must be destroyed; when the status is not OK
+ * it carries the error (b200lu_analysis_status / _message) and no product. RowLookupTable, the CPU
+ * elimination's per-row hash/bitmap, is not part of the product: the device path does not use it. */
+typedef struct b200lu_analysis b200lu_analysis;
+b200lu_status b200lu_analyze(int64_t n, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
+                             int use_scaling, int use_amd, b200lu_analysis** out);
+/* Status of the analysis; failed_row = ZeroDiagonalError::row (a row of the permuted matrix B, as the
+ * reference reports it) or the first deficient row; deficient_rows = StructurallySingularError::deficient_rows
+ * (borrowed, sorted). Any out pointer may be NULL. */
+b200lu_status b200lu_analysis_status(const b200lu_analysis* a, int64_t* failed_row, const int64_t** deficient_rows,
+                                     int64_t* deficient_count);
+const char* b200lu_analysis_message(const b200lu_analysis* a);
+/* The product as the view b200lu_create / b200lu_batch_create consume; pointers are borrowed from the
+ * analysis object. fill_count (may be NULL) = SymbolicFactors::fill_count. */
+b200lu_status b200lu_analysis_view(const b200lu_analysis* a, b200lu_symbolic_view* view, int64_t* fill_count);
+/* Host milliseconds spent in {matching, ordering, permutation, fill pattern, scatter map, total};
+ * matched_product (may be NULL) = MatchingResult::matched_product. */
+b200lu_status b200lu_analysis_times(const b200lu_analysis* a, double* ms_out6, double* matched_product);
+void b200lu_analysis_destroy(b200lu_analysis* a);
 
 #ifdef __cplusplus
 }

@@ -225,6 +225,58 @@ inline RefineOutcome classic_refine(const NumericFactors& f, const DenseVector& 
 }
 
 // ---------------------------------------------------------------------------------------------
+// Host-side symbolic analysis (b200lu_analyze, csrc/analyze.cpp): rlu::symbolic_analyze(A, AnalyzeOptions)
+// (include/rlu/symbolic.hpp:67-75, src/symbolic.cpp:156-203) — the same product bit for bit, owned by this object.
+class ZeroDiagonalError : public Error {  // include/rlu/errors.hpp:37-42
+ public:
+  ZeroDiagonalError(const std::string& msg, std::int64_t r) : Error(msg), row(r) {}
+  std::int64_t row;
+};
+class StructurallySingularError : public Error {  // include/rlu/errors.hpp:27-34
+ public:
+  StructurallySingularError(const std::string& msg, std::vector<std::int64_t> rows) : Error(msg), deficient_rows(std::move(rows)) {}
+  std::vector<std::int64_t> deficient_rows;
+};
+struct AnalyzeOptions {  // include/rlu/symbolic.hpp:67-70
+  bool use_scaling = true;
+  bool use_amd = true;
+};
+class SymbolicAnalysis {
+ public:
+  SymbolicAnalysis(const CsrMatrix& A, const AnalyzeOptions& opt = {}) {
+    if (A.nrows != A.ncols) throw DimensionError("symbolic_analyze: matrix must be square");
+    if (static_cast<index_t>(A.row_offsets.size()) != A.nrows + 1) throw Error("row_offsets length must be nrows + 1");
+    if (opt.use_scaling && !(A.has_values() && !A.values.empty())) throw Error("mc64_scale: matrix has no values");
+    const b200lu_status st = b200lu_analyze(A.nrows, A.row_offsets.data(), A.col_indices.data(),
+                                            opt.use_scaling ? A.values.data() : nullptr, opt.use_scaling, opt.use_amd, &h_);
+    if (!h_) throw Error(std::string("symbolic_analyze: ") + b200lu_status_string(st));
+    if (st != B200LU_OK) {
+      std::int64_t row = -1, count = 0;
+      const std::int64_t* rows = nullptr;
+      b200lu_analysis_status(h_, &row, &rows, &count);
+      const std::string msg = b200lu_analysis_message(h_);
+      std::vector<std::int64_t> deficient(rows, rows + count);
+      b200lu_analysis_destroy(h_);
+      h_ = nullptr;
+      if (st == B200LU_ZERO_DIAGONAL) throw ZeroDiagonalError(msg, row);
+      if (st == B200LU_STRUCTURALLY_SINGULAR) throw StructurallySingularError(msg, std::move(deficient));
+      throw Error(msg);
+    }
+    b200lu_analysis_view(h_, &view_, &fill_count_);
+  }
+  SymbolicAnalysis(const SymbolicAnalysis&) = delete;
+  SymbolicAnalysis& operator=(const SymbolicAnalysis&) = delete;
+  ~SymbolicAnalysis() { b200lu_analysis_destroy(h_); }
+  const SymbolicView& view() const { return view_; }  // valid while this object lives
+  index_t fill_count() const { return fill_count_; }
+
+ private:
+  b200lu_analysis* h_ = nullptr;
+  SymbolicView view_{};
+  std::int64_t fill_count_ = 0;
+};
+
+// ---------------------------------------------------------------------------------------------
 // Scenario batches (b200lu_batch_*): `batch` systems over one SymbolicView, factorized and solved
 // together. Arrays are scenario-major: values [batch][nnz(A)], vectors [batch][n].
 class BatchedFactors {

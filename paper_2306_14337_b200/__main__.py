@@ -1,7 +1,7 @@
 """`python -m paper_2306_14337_b200` — the device-path counterpart of the reference's `rlu` CLI
 (proj/src/cli.cpp:216-321; same subcommands, option names, report formats and exit codes where they apply):
 
-    solve-seq --input MANIFEST --analyzer MODULE:FUNCTION [--scaling mc64|none] [--ordering amd|natural]
+    solve-seq --input MANIFEST [--analyzer MODULE:FUNCTION] [--scaling mc64|none] [--ordering amd|natural]
               [--refine fgmres|classic|none] [--refine-tol T] [--refine-maxit N] [--format json|csv] [--out PATH]
               [--device D]
     report    REPORT.json [--format json|csv] [--out PATH]
@@ -11,11 +11,11 @@ src/io.cpp:25-87), runs cli::solve_sequence's loop (analyze once, refactorize + 
 escalation on failure: sequence.py) on the GPU and writes the SolveReport with the reference's field names
 (src/report.cpp:30-119). Exit code 0 when every system was solved, 2 otherwise, 1 on an error — cli.cpp:304-318.
 
-The symbolic analysis (MC64, AMD, fill pattern) is the reference's own host code and is not part of this
-package: `--analyzer` names the callable that provides it,
+The symbolic analysis (MC64, AMD, fill pattern) defaults to the package's own host code (analysis.py over
+csrc/analyze.cpp: the reference's product bit for bit); `--analyzer` substitutes another provider,
 `analyze(K: CsrMatrix, use_scaling: bool, use_amd: bool) -> SymbolicFactors` — e.g. a thin binding of the
-reference's symbolic_analyze. There is no `gen` subcommand for the same reason (the generator is the
-reference's); sequences written by `rlu gen --out DIR` load unchanged.
+reference's symbolic_analyze. There is no `gen` subcommand (the generator is the reference's); sequences
+written by `rlu gen --out DIR` load unchanged.
 """
 from __future__ import annotations
 
@@ -46,13 +46,19 @@ def _load_callable(spec: str):
     return getattr(importlib.import_module(mod), fn)
 
 
+def _builtin_analyze(K, use_scaling: bool, use_amd: bool):
+    from .analysis import AnalyzeOptions, symbolic_analyze
+    return symbolic_analyze(K, AnalyzeOptions(use_scaling, use_amd))
+
+
 def run_cli(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2306_14337_b200",
                                  description="sparse LU refactorization solver for fixed-pattern KKT sequences (B200 path)")
     sub = ap.add_subparsers(dest="cmd", required=True)
     solve = sub.add_parser("solve-seq", help="solve a sequence, analyzing once and refactorizing the rest")
     solve.add_argument("--input", required=True, help="sequence manifest file")
-    solve.add_argument("--analyzer", required=True, help="MODULE:FUNCTION providing the host-side symbolic analysis")
+    solve.add_argument("--analyzer", default="", help="MODULE:FUNCTION providing the host-side symbolic analysis "
+                       "(default: the built-in analysis)")
     solve.add_argument("--scaling", default="mc64", choices=["mc64", "none"])
     solve.add_argument("--ordering", default="amd", choices=["amd", "natural"])
     solve.add_argument("--refine", default="none", choices=["fgmres", "classic", "none"])
@@ -71,7 +77,7 @@ def run_cli(argv=None) -> int:
         return 0 if e.code == 0 else 1
     try:
         if args.cmd == "solve-seq":
-            analyze = _load_callable(args.analyzer)
+            analyze = _load_callable(args.analyzer) if args.analyzer else _builtin_analyze
             systems = load_sequence(args.input)
             opt = PipelineOptions(use_scaling=args.scaling == "mc64", use_amd=args.ordering == "amd", refine=args.refine,
                                   refine_tol=args.refine_tol, refine_maxit=args.refine_maxit, device=args.device)

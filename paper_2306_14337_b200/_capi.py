@@ -10,7 +10,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libb200lu.so")
 
-OK, ZERO_PIVOT, PATTERN_MISMATCH, DIMENSION, INVALID_FACTORS, CUDA_ERROR, INVALID_ARGUMENT, NO_DEVICE = range(8)
+(OK, ZERO_PIVOT, PATTERN_MISMATCH, DIMENSION, INVALID_FACTORS, CUDA_ERROR, INVALID_ARGUMENT, NO_DEVICE, ZERO_DIAGONAL,
+ STRUCTURALLY_SINGULAR) = range(10)
 
 i64, u64, dbl, i32, vp = C.c_int64, C.c_uint64, C.c_double, C.c_int, C.c_void_p
 
@@ -121,6 +122,13 @@ EXPORTS = {
     "b200lu_batch_set_timing": (i32, [vp, i32]),
     "b200lu_batch_get_phase_times": (i32, [vp, C.POINTER(dbl), C.POINTER(i64), i32]),
     "b200lu_batch_synchronize": (i32, [vp]),
+    # host-side symbolic analysis
+    "b200lu_analyze": (i32, [i64, vp, vp, vp, i32, i32, C.POINTER(vp)]),
+    "b200lu_analysis_status": (i32, [vp, C.POINTER(i64), C.POINTER(vp), C.POINTER(i64)]),
+    "b200lu_analysis_message": (C.c_char_p, [vp]),
+    "b200lu_analysis_view": (i32, [vp, C.POINTER(SymbolicView), C.POINTER(i64)]),
+    "b200lu_analysis_times": (i32, [vp, C.POINTER(dbl), C.POINTER(dbl)]),
+    "b200lu_analysis_destroy": (None, [vp]),
 }
 
 FLAG_STRICT_ORDER = 1

@@ -725,6 +725,8 @@ const char* b200lu_status_string(b200lu_status s) {
     case B200LU_CUDA_ERROR: return "CUDA error";
     case B200LU_INVALID_ARGUMENT: return "invalid argument";
     case B200LU_NO_DEVICE: return "no CUDA device";
+    case B200LU_ZERO_DIAGONAL: return "structurally zero diagonal";
+    case B200LU_STRUCTURALLY_SINGULAR: return "structurally singular";
   }
   return "unknown";
 }

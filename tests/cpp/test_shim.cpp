@@ -116,6 +116,38 @@ int main() {
     CHECK(f.valid() && f.generation() == 1);
   });
 
+  run("SymbolicAnalysis: natural-order product == symbolic elimination; MC64 + AMD product factorizes and solves", [] {
+    const Dense M = {{4, 1, 0, 1, 0}, {1, 5, 2, 0, 0}, {0, 2, 6, 0, 1}, {1, 0, 0, 7, 3}, {0, 0, 1, 3, 8}};
+    Sym s(M);
+    SymbolicAnalysis plain(s.A, AnalyzeOptions{false, false});
+    const SymbolicView& v = plain.view();
+    CHECK(v.nnz_factors == s.view.nnz_factors && v.col_perm_forward == nullptr);
+    for (index_t k = 0; k < v.nnz_factors; ++k) CHECK(v.col_indices[k] == s.ci[k]);
+    for (index_t i = 0; i < s.n; ++i) CHECK(v.diag_pos[i] == s.dp[i] && v.amd_forward[i] == i);
+    for (index_t k = 0; k < v.nnz_source; ++k) CHECK(v.scatter_map[k] == s.smap[k] && v.scatter_scale[k] == 1.0);
+    CHECK(plain.fill_count() == v.nnz_factors - v.nnz_source);
+    SymbolicAnalysis full(s.A);  // use_scaling = use_amd = true, the reference's defaults
+    NumericFactors f = factorize(full.view(), s.A);
+    const DenseVector xt = {1, -2, 3, -4, 5};
+    DenseVector b(5, 0.0);
+    for (int i = 0; i < 5; ++i)
+      for (int j = 0; j < 5; ++j) b[i] += M[i][j] * xt[j];
+    const DenseVector x = solve_system(f, b);
+    for (int i = 0; i < 5; ++i) CHECK(std::fabs(x[i] - xt[i]) <= 1e-13);
+    bool threw = false;
+    try {
+      CsrMatrix Z = s.A;  // drop the (2, 2) entry: structurally zero diagonal (src/symbolic.cpp:121-123)
+      const index_t pos = Z.row_offsets[2] + 1;
+      Z.col_indices.erase(Z.col_indices.begin() + pos);
+      Z.values.erase(Z.values.begin() + pos);
+      for (index_t i = 3; i <= 5; ++i) Z.row_offsets[i]--;
+      SymbolicAnalysis bad(Z, AnalyzeOptions{false, false});
+    } catch (const ZeroDiagonalError& e) {
+      threw = e.row == 2;
+    }
+    CHECK(threw);
+  });
+
   run("scatter zeroes exactly the fill slots; pattern change is rejected (test_numeric.cpp:105-123)", [] {
     Sym s({{4, 1, 1, 1}, {1, 3, 0, 0}, {1, 0, 3, 0}, {1, 0, 0, 3}});
     NumericFactors f(s.view);

@@ -101,8 +101,9 @@ def _ref_analyze(K, use_scaling, use_amd):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scaling,refine", [("none", "fgmres"), ("mc64", "classic")])
-def test_solve_seq_from_disk_meets_the_acceptance_checks(tmp_path, scaling, refine):
+@pytest.mark.parametrize("scaling,refine,analyzer", [("none", "fgmres", "reference"), ("mc64", "classic", "reference"),
+                                                     ("none", "fgmres", "builtin"), ("mc64", "fgmres", "builtin")])
+def test_solve_seq_from_disk_meets_the_acceptance_checks(tmp_path, scaling, refine, analyzer):
     from oracle import refbridge as rb
     if not rb.available():
         pytest.skip("oracle/_ref/librlu_ref.so not built")
@@ -111,7 +112,9 @@ def test_solve_seq_from_disk_meets_the_acceptance_checks(tmp_path, scaling, refi
     mmio.write_sequence([KktSystem(rlu.CsrMatrix(q.n, q.n, ro, ci, q.values(k)), q.rhs(k), k, q.mu(k)) for k in range(len(q))],
                         str(tmp_path / "seq"))
     out = tmp_path / "report.json"
-    rc = run_cli(["solve-seq", "--input", str(tmp_path / "seq" / "manifest.txt"), "--analyzer", "tests.test_cli_io:_ref_analyze",
+    # the built-in analysis (csrc/analyze.cpp) is the default; the reference's own is the substitute provider
+    provider = ["--analyzer", "tests.test_cli_io:_ref_analyze"] if analyzer == "reference" else []
+    rc = run_cli(["solve-seq", "--input", str(tmp_path / "seq" / "manifest.txt"), *provider,
                   "--scaling", scaling, "--refine", refine, "--out", str(out)])
     assert rc == 0
     rep = SolveReport.from_json(out.read_text())
