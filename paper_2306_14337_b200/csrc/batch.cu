@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -21,6 +22,7 @@
 #include "batch.cuh"
 #include "schedule.hpp"
 #include "tile.cuh"
+#include "gather.cuh"
 
 using namespace b200lu;
 
@@ -92,6 +94,17 @@ struct b200lu_batch {
   int tile_grid = 0;
   size_t tile_smem = 0;
   BTileArgs tile_args;
+  // gather-form trailing part (gather.cuh): register accumulation per (target, batch of pivots)
+  bool use_gather = false;
+  GBlock* d_g_blocks = nullptr;
+  GBatch* d_g_batches = nullptr;
+  GRec* d_g_recs = nullptr;
+  int32_t* d_g_waits = nullptr;
+  int32_t n_g_blocks = 0, gather_rows_per = 2, gather_batch = 16;
+  int64_t gather_records = 0, gather_targets = 0;
+  void (*gather_fn)(BGatherArgs) = nullptr;
+  int gather_grid = 0;
+  size_t gather_smem = 0;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
@@ -309,7 +322,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
         cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
     ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
   }
-  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0 || h->n_tiles > 0) {
+  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0 || h->n_tiles > 0 || h->n_g_blocks > 0) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
@@ -342,6 +355,26 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       ta.ticket = h->d_tickets + 1;
       h->tile_fn<<<h->tile_grid, (h->tile_rows_per + 1) * 32, h->tile_smem, h->stream>>>(ta);
       ST_TRY(check_launch(h, "bfactor_tile_kernel"));
+    }
+    if (h->use_gather && h->n_g_blocks > 0) {
+      BGatherArgs ga;
+      ga.n_blocks = h->n_g_blocks;
+      ga.units = h->units;
+      ga.gen = h->gen;
+      ga.blocks = h->d_g_blocks;
+      ga.batches = h->d_g_batches;
+      ga.recs = h->d_g_recs;
+      ga.waits = h->d_g_waits;
+      ga.diag = h->d_diag;
+      ga.values = h->d_values;
+      ga.nnz_factors = h->nnz_factors;
+      ga.flags = h->d_flags;
+      ga.pivot_floor = h->pivot_floor;
+      ga.failed = h->d_failed;
+      ga.ticket = h->d_tickets + 1;
+      ga.exp_nowait = std::getenv("B200LU_GATHER_NOWAIT") ? 1 : 0;
+      h->gather_fn<<<h->gather_grid, 256, h->gather_smem, h->stream>>>(ga);
+      ST_TRY(check_launch(h, "bfactor_gather_kernel"));
     }
     if (h->n_blocks > 0) {
       BBlockArgs bb;
@@ -1065,6 +1098,60 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
         tail_rows.clear();
       }
     }
+    //   * bfactor_gather_kernel (gather.cuh): R-row blocks x 32 scenarios; every target entry a batch of K pivots
+    //     touches is loaded once, updated in a register and stored once: no L2 reductions at all.
+    //     Bit-exact, and it does what it was built for — ncu at C2 x 256: L2 reductions 0, DRAM traffic 40 GB
+    //     against 47 GB — but it LOSES: 85-105 ms against 24.4 ms for the row-blocked kernel (57 ms at 32 scenarios
+    //     against 8.2 / 4.9 ms). The record interpreter costs 53 warp instructions per record (two index words,
+    //     a type switch the compiler cannot prove warp-uniform, 64-bit address arithmetic: 14.5 G instructions per
+    //     refactorization against 5.7 G), and the trailing DAG is narrow (16 439 rows in 925 levels): the time
+    //     is levels x (latency of one warp walking one batch), and a batch's loads are only one chunk deep.
+    //     Without the flag waits (timing experiment B200LU_GATHER_NOWAIT, wrong results) it still takes 50 ms.
+    //     Kept as an experiment, OFF by default.
+    // B200LU_BATCH_GATHER = 1 selects it (with B200LU_BATCH_TILES = 0 for small batches);
+    // B200LU_GATHER_R (1, 2, 4), B200LU_GATHER_K (8, 16, 32), B200LU_GATHER_SMALL (pivots of the last, short batch).
+    e = std::getenv("B200LU_BATCH_GATHER");
+    const bool want_gather = e ? std::atoi(e) != 0 : false;
+    if (want_gather && !tail_rows.empty() && tail_mode != 0) {
+      e = std::getenv("B200LU_GATHER_R");
+      const int gr = e ? std::atoi(e) : 2;
+      e = std::getenv("B200LU_GATHER_K");
+      const int gk = e ? std::atoi(e) : 16;
+      e = std::getenv("B200LU_GATHER_SMALL");
+      const int gs = e ? std::atoi(e) : 2;
+      GatherPlan plan;
+      std::string err;
+      int gr_used = gr, gk_used = gk;
+      if (!build_gather_plan(S.row_ptr, S.col, S.diag, S.lower_level, tail_rows, gr, gk, gs, &plan, &err)) {
+        // blocks of several rows can depend on each other both ways when the trailing rows are not
+        // index-consecutive; single-row blocks cannot
+        gr_used = 1;
+        gk_used = 32;
+        if (!build_gather_plan(S.row_ptr, S.col, S.diag, S.lower_level, tail_rows, gr_used, gk_used, gs, &plan, &err)) {
+          h->last_error = err;
+          return B200LU_INVALID_ARGUMENT;
+        }
+      }
+      ST_TRY(dev_upload(h, &h->d_g_blocks, plan.blocks));
+      ST_TRY(dev_upload(h, &h->d_g_batches, plan.batches));
+      ST_TRY(dev_upload(h, &h->d_g_recs, plan.recs));
+      ST_TRY(dev_upload(h, &h->d_g_waits, plan.waits));
+      h->use_gather = true;
+      h->n_g_blocks = static_cast<int32_t>(plan.blocks.size());
+      h->gather_rows_per = gr_used;
+      h->gather_batch = gk_used;
+      h->gather_records = static_cast<int64_t>(plan.recs.size());
+      h->gather_targets = plan.n_targets;
+      if (std::getenv("B200LU_GATHER_VERBOSE")) {
+        std::fprintf(stderr, "gather plan: R %d K %d rows %lld blocks %zu batches %zu records %zu (init %lld upd %lld div %lld pub %lld pad %lld) targets %lld waits %zu\n",
+                     gr_used, gk_used, static_cast<long long>(plan.rows), plan.blocks.size(), plan.batches.size(), plan.recs.size(),
+                     static_cast<long long>(plan.n_init), static_cast<long long>(plan.n_upd), static_cast<long long>(plan.n_div),
+                     static_cast<long long>(plan.n_pub), static_cast<long long>(plan.n_pad), static_cast<long long>(plan.n_targets), plan.waits.size());
+      }
+      h->n_block_rows = static_cast<int32_t>(tail_rows.size());
+      for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+      tail_rows.clear();
+    }
     std::vector<BlockMeta> blocks;
     std::vector<MergedPivot> merged;
     for (size_t b0 = 0; b0 < tail_rows.size(); b0 += kBlockRows) {
@@ -1274,6 +1361,29 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     int bocc = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, h->block_smem));
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
+    if (h->use_gather) {
+      using GFn = void (*)(BGatherArgs);
+      const char* em = std::getenv("B200LU_GATHER_MINB");
+      const int minb = em ? std::atoi(em) : 2;
+      const int gr = h->gather_rows_per, gk = h->gather_batch;
+      GFn gfn = nullptr;
+      if (gr == 2 && gk == 16) gfn = minb >= 3 ? bfactor_gather_kernel<2, 16, 3> : bfactor_gather_kernel<2, 16, 2>;
+      if (gr == 2 && gk == 8) gfn = minb >= 3 ? bfactor_gather_kernel<2, 8, 3> : bfactor_gather_kernel<2, 8, 2>;
+      if (gr == 2 && gk == 32) gfn = bfactor_gather_kernel<2, 32, 2>;
+      if (gr == 4 && gk == 8) gfn = minb >= 3 ? bfactor_gather_kernel<4, 8, 3> : bfactor_gather_kernel<4, 8, 2>;
+      if (gr == 4 && gk == 16) gfn = bfactor_gather_kernel<4, 16, 2>;
+      if (gr == 1 && gk == 32) gfn = minb >= 3 ? bfactor_gather_kernel<1, 32, 3> : bfactor_gather_kernel<1, 32, 2>;
+      if (!gfn) {
+        h->last_error = "gather kernel: unsupported (R, K) combination";
+        return B200LU_INVALID_ARGUMENT;
+      }
+      h->gather_fn = gfn;
+      h->gather_smem = gather_smem_bytes(gr, gk, 8);
+      CU_TRY(h, cudaFuncSetAttribute(gfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->gather_smem)));
+      int gocc = 0;
+      CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gocc, gfn, 256, h->gather_smem));
+      h->gather_grid = prop.multiProcessorCount * std::max(1, gocc);
+    }
   }
   {
     int o1 = 0, o2 = 0, o3 = 0;
@@ -1317,7 +1427,7 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_tile_prof, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_g_blocks, h->d_g_batches, h->d_g_recs, h->d_g_waits, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_tile_prof, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
                   h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
@@ -1700,7 +1810,7 @@ b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* ou
   out->unit_scenarios = h->unit;
   out->factor_rows = h->n_factor_rows + h->n_block_rows;
   out->blocked_rows = h->n_block_rows;
-  out->blocks = h->use_tiles ? h->n_tiles : h->n_blocks;
+  out->blocks = h->use_tiles ? h->n_tiles : h->use_gather ? h->n_g_blocks : h->n_blocks;
   out->blocked_pairs = h->blocked_pairs;
   out->factor_grid = h->factor_grid;
   out->tri_grid = h->tri_grid;

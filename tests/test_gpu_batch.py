@@ -114,6 +114,29 @@ def test_batch_trailing_part_variants(width, mode, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("rows,batch_len,small", [(2, 16, 1), (2, 8, 2), (4, 8, 1), (1, 32, 1), (2, 32, 0)])
+def test_batch_gather_form_is_bit_exact(rows, batch_len, small, monkeypatch):
+    """The experimental gather form of the trailing refactorization (csrc/gather.cuh: every target entry a batch
+    of pivots touches is loaded once, updated in a register in ascending pivot order, stored once — no L2
+    reductions). Slower than the default kernels and off by default; its results are the
+    reference's bit for bit, with and without MC64, including a zero-pivot scenario."""
+    monkeypatch.setenv("B200LU_BATCH_GATHER", "1")
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    monkeypatch.setenv("B200LU_GATHER_R", str(rows))
+    monkeypatch.setenv("B200LU_GATHER_K", str(batch_len))
+    monkeypatch.setenv("B200LU_GATHER_SMALL", str(small))
+    fx = kkt_fixture(700, 300, num_systems=4)
+    f = BatchedFactors(fx.sym, 17)
+    info = f.info
+    f.close()
+    assert info["blocks"] > 0 and info["blocked_rows"] > 0 and not info["tiled"]
+    _check_batch(fx, 17, refine=False)
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+
+
+@needs_ref
 def test_batch_long_pivot_rows_cross_chunks():
     """A banded matrix with 40 upper entries per row: every pivot row spans several load batches."""
     n, band = 400, 40
