@@ -193,6 +193,24 @@ def calibrate_reference(ref_sym, seq, rb):
     return num, best
 
 
+
+def analyze_for_bench(rlu, rb, A, np):
+    """Host-side symbolic analysis of the workload (untimed part of the fixture): the package's own
+    b200lu_analyze (csrc/analyze.cpp) provides the product the GPU path runs on; the reference's symbolic_analyze
+    (needed anyway by the CPU baseline) is compared with it array by array. Returns (sym, ref_sym, report)."""
+    ro, ci, va = A.arrays()
+    sym, tm = rlu.symbolic_analyze(rlu.CsrMatrix(A.n, A.n, ro, ci, va), rlu.AnalyzeOptions(False, True), with_times=True)
+    ref_sym = rb.RefSymbolic(A, use_scaling=False, use_amd=True)
+    r = ref_sym.arrays()
+    same = all(np.array_equal(np.asarray(getattr(sym, k)), np.asarray(getattr(r, k)))
+               for k in ("row_offsets", "col_indices", "diag_pos", "scatter_map", "scatter_scale", "amd_forward"))
+    if not same:
+        raise SystemExit("bench.py: b200lu_analyze and the reference's symbolic_analyze disagree")
+    return sym, ref_sym, {"b200lu_analyze_ms": round(tm.total_ms, 1), "reference_symbolic_analyze_ms": round(ref_sym.analyze_ms, 1),
+                          "identical_product": True, "host_threads": 1,
+                          "stages_ms": {"ordering": round(tm.ordering_ms, 1), "fill": round(tm.fill_ms, 1),
+                                        "scatter_map": round(tm.scatter_map_ms, 1)}}
+
 def run_reference(args):
     """--impl reference: the unmodified reference CPU path on this box's host cores."""
     rank, _, world = dist_env()
@@ -250,8 +268,7 @@ def measure_single(args, workload, steps, with_cpu_baseline):
     n, m, desc = WORKLOADS[workload]
     # ---- input fixture (untimed): the reference's generator + host-side symbolic analysis
     seq = rb.RefSequence(n, m, y_seed=2 + rank)
-    ref_sym = rb.RefSymbolic(seq.matrix(0), use_scaling=False, use_amd=True)
-    sym = rlu.SymbolicFactors.from_arrays(ref_sym.arrays())
+    sym, ref_sym, analysis = analyze_for_bench(rlu, rb, seq.matrix(0), np)
     ro, ci = seq.pattern()
     nsys = len(seq)
     N, nnz_a, nnz_f = seq.n, seq.nnz, ref_sym.nnz_factors
@@ -371,6 +388,7 @@ def measure_single(args, workload, steps, with_cpu_baseline):
                 "note": "values + rhs from pinned host memory H2D and x D2H inside the timed region, through "
                         "the public refactorize/solve_system/fgmres_refine calls"},
         "gpu_launches": launches,
+        "analysis": analysis,
         "phases_ms_per_step": {p: v[0] / steps for p, v in phases.items()},
         "launches_per_step": {p: v[1] / steps for p, v in phases.items()},
         "refine_iters_median": med_iters, "relres_final_max": relres_max,
@@ -474,8 +492,7 @@ def run_batch(args):
     S_max = -(-total_scen // world)
     # ---- input fixture (untimed): one generated scenario per y_seed, one symbolic analysis
     seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1, keep_blocks=True) for sc in mine]
-    ref_sym = rb.RefSymbolic(seqs[0].matrix(0), use_scaling=False, use_amd=True)
-    sym = rlu.SymbolicFactors.from_arrays(ref_sym.arrays())
+    sym, ref_sym, analysis = analyze_for_bench(rlu, rb, seqs[0].matrix(0), np)
     ro, ci = seqs[0].pattern()
     N, nnz_a, nnz_f = seqs[0].n, seqs[0].nnz, ref_sym.nnz_factors
     diag_pos = np.nonzero(np.repeat(np.arange(N), np.diff(ro)) == ci)[0]
@@ -671,6 +688,7 @@ def run_batch(args):
                         "SURVEY 8f-1): the scenarios share H and J, so only each scenario's barrier diagonal D_y "
                         "(n_primal doubles) and rhs are copied H2D and K's diagonal is rewritten on the device"},
             "gpu_launches": launches,
+            "analysis": analysis,
             "phases_ms_per_step": {p: v[0] / args.steps for p, v in phases.items()},
             "launches_per_step": {p: v[1] / args.steps for p, v in phases.items()},
             "refine_iters_median": med_iters, "relres_final_max_vs_reference_residual": relres_max,
@@ -699,8 +717,10 @@ def run_batch(args):
                 "relres_final_max", "roofline", "gpu_launches")
         if single is not None:
             line["single_system"] = {k: single[k] for k in keys}
+            line["single_system"]["analysis"] = single.get("analysis")
         if c4 is not None:
             line["c4"] = {k: c4[k] for k in keys}
+            line["c4"]["analysis"] = c4.get("analysis")
         if nccl_lines is not None:
             line["nccl"] = nccl_lines
         if not args.no_cpu_baseline:  # rank 0, at every N: the reference on this box's host cores
