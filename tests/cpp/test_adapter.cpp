@@ -23,15 +23,44 @@ static int fail(const char* what) {
 }
 
 int main(int argc, char** argv) {
-  if (b200lu_device_count() == 0) {
-    std::printf("no CUDA device: the b200 backend has no CPU fallback\n");
-    return 3;
-  }
   GenConfig cfg;
   cfg.n = argc > 1 ? std::atoll(argv[1]) : 1400;
   cfg.m = argc > 2 ? std::atoll(argv[2]) : 600;
   cfg.num_systems = 10;
   const KktSequence seq = gen_sequence(cfg);
+  // symbolic_analyze through the adapter (b200lu_analyze) against the reference's own, field by field, with and
+  // without MC64 — the values of the matching's scale factors compared bitwise (src/symbolic.cpp:156-203)
+  for (const bool scaling : {false, true}) {
+    AnalyzeOptions o;
+    o.use_scaling = scaling;
+    const SymbolicFactors want = symbolic_analyze(seq.systems[0].K, o);
+    const SymbolicFactors got = b200::symbolic_analyze(seq.systems[0].K, o, /*with_row_lookup=*/true);
+    bool same = got.n == want.n && got.combined_pattern.row_offsets == want.combined_pattern.row_offsets &&
+                got.combined_pattern.col_indices == want.combined_pattern.col_indices && got.diag_pos == want.diag_pos &&
+                got.scatter_map == want.scatter_map && got.amd.forward == want.amd.forward && got.amd.inverse == want.amd.inverse &&
+                got.fill_count == want.fill_count && got.match.has_value() == want.match.has_value() &&
+                got.scatter_scale.size() == want.scatter_scale.size() &&
+                std::memcmp(got.scatter_scale.data(), want.scatter_scale.data(), got.scatter_scale.size() * sizeof(double)) == 0;
+    if (same && want.match) {
+      same = got.match->col_perm.forward == want.match->col_perm.forward &&
+             std::memcmp(got.match->scaling.row_scale.data(), want.match->scaling.row_scale.data(), sizeof(double) * want.n) == 0 &&
+             std::memcmp(got.match->scaling.col_scale.data(), want.match->scaling.col_scale.data(), sizeof(double) * want.n) == 0 &&
+             got.match->matched_product == want.match->matched_product;
+    }
+    if (!same) return fail("b200::symbolic_analyze differs from the reference's symbolic_analyze");
+    // and the product is a full SymbolicFactors: the reference's own CPU factorization runs on it
+    const auto shared = std::make_shared<const SymbolicFactors>(got);
+    NumericFactors on_fast(shared, FactorOptions{});
+    NumericFactors on_ref(std::make_shared<const SymbolicFactors>(want), FactorOptions{});
+    refactorize(on_fast, seq.systems[0].K);
+    refactorize(on_ref, seq.systems[0].K);
+    if (on_fast.values != on_ref.values) return fail("reference factorization on the adapter's analysis differs");
+    std::printf("ok symbolic_analyze (%s): identical product, fill %lld\n", scaling ? "mc64 + amd" : "amd", static_cast<long long>(got.fill_count));
+  }
+  if (b200lu_device_count() == 0) {
+    std::printf("no CUDA device: the b200 backend has no CPU fallback\n");
+    return 3;
+  }
   AnalyzeOptions aopt;
   aopt.use_scaling = false;  // the KLU-style path of the north star (cli.hpp:14)
   const auto sym = std::make_shared<const SymbolicFactors>(symbolic_analyze(seq.systems[0].K, aopt));

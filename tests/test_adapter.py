@@ -21,6 +21,9 @@ def test_adapter_builds_and_refuses_without_a_device():
         pytest.skip("a device is present")
     r = subprocess.run([EXE], capture_output=True, text=True)
     assert r.returncode == 3 and "no CUDA device" in r.stdout
+    # the host-side part runs without a device: rlu::b200::symbolic_analyze == the reference's symbolic_analyze, field by
+    # field, with and without MC64, and the reference's own CPU factorization runs on its product
+    assert r.stdout.count("ok symbolic_analyze") == 2
 
 
 @needs_exe
@@ -30,4 +33,4 @@ def test_adapter_sequence_bitwise_on_device(shape):
     r = subprocess.run([EXE, *shape], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all ok" in r.stdout and r.stdout.count("L/U bitwise") == 10
-    assert "ok cgs2" in r.stdout and "ok errors" in r.stdout
+    assert "ok cgs2" in r.stdout and "ok errors" in r.stdout and r.stdout.count("ok symbolic_analyze") == 2
