@@ -511,10 +511,12 @@ b200lu_status any_valid(H* h, const char* who) {
 b200lu_status launch_residual(H* h, const double* x, const double* b, double* r, int slot) {
   {
     PhaseScope ps(h, B200LU_PHASE_SPMV);
+    bresidual_rows_kernel<<<warp_blocks(h), 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->groups, h->nnz_source,
+                                                               h->d_a_row_ptr, h->d_a_col, h->d_a_int, x, b, r);
+    ST_TRY(check_launch(h, "bresidual_rows_kernel"));
     dim3 grid(kBatchPartBlocks, static_cast<unsigned>(h->groups));
-    bresidual_kernel<<<grid, 256, 0, h->stream>>>(static_cast<int32_t>(h->n), h->nnz_source, h->d_a_row_ptr, h->d_a_col,
-                                                  h->d_a_int, x, b, r, h->d_partials);
-    ST_TRY(check_launch(h, "bresidual_kernel"));
+    bsumsq2_kernel<<<grid, 256, 0, h->stream>>>(static_cast<int32_t>(h->n), r, b, h->d_partials);
+    ST_TRY(check_launch(h, "bsumsq2_kernel"));
   }
   PhaseScope ps(h, B200LU_PHASE_VECTOR);
   bfinish_kernel<<<h->groups, 32, 0, h->stream>>>(2, h->padded, h->d_partials, scal(h, slot));

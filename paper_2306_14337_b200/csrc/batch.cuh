@@ -829,27 +829,53 @@ __device__ __forceinline__ void brow_range(int32_t n, int32_t& i0, int32_t& i1) 
   i1 = min(n, i0 + per);
 }
 
-// r = b - A x (spmv, src/sparse.cpp:135-141: left-to-right accumulation per row) with the
-// partial sums of r^2 and b^2 (relative_residual, src/sparse.cpp:283-288).
+// r = b - A x (spmv, src/sparse.cpp:135-141: left-to-right accumulation per row), one warp per (row, group): the
+// gathers of a row are dependent loads, so the rows must run side by side, not one after the other.
 __global__ void __launch_bounds__(256)
-bresidual_kernel(int32_t n, int64_t nnz_source, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                 const double* __restrict__ a_int, const double* __restrict__ x, const double* __restrict__ b,
-                 double* __restrict__ r, double* __restrict__ partials) {
+bresidual_rows_kernel(int32_t n, int32_t groups, int64_t nnz_source, const int32_t* __restrict__ row_ptr,
+                      const int32_t* __restrict__ col, const double* __restrict__ a_int, const double* __restrict__ x,
+                      const double* __restrict__ b, double* __restrict__ r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= static_cast<int64_t>(n) * groups) return;
+  const int64_t g = warp / n, i = warp - g * n;
+  const double* ag = a_int + g * nnz_source * 32 + lane;
+  const double* xg = x + g * n * 32 + lane;
+  double acc = 0.0;
+  for (int32_t k = __ldg(row_ptr + i); k < __ldg(row_ptr + i + 1); ++k) {
+    acc = add_prod(acc, ag[static_cast<int64_t>(k) * 32], xg[static_cast<int64_t>(__ldg(col + k)) * 32]);
+  }
+  r[warp * 32 + lane] = __dsub_rn(b[warp * 32 + lane], acc);
+}
+
+// Partial sums of r^2 and b^2 (relative_residual, src/sparse.cpp:283-288) in the fixed geometry of the
+// per-scenario reductions: every warp folds its block of rows in row order (loads of 8 rows in flight, the
+// additions in order), so the sums are the ones the fused kernel of round 1 produced, bit for bit.
+__global__ void __launch_bounds__(256)
+bsumsq2_kernel(int32_t n, const double* __restrict__ r, const double* __restrict__ b, double* __restrict__ partials) {
   const int lane = threadIdx.x & 31;
   const int64_t g = blockIdx.y;
   int32_t i0, i1;
   brow_range(n, i0, i1);
-  const double* ag = a_int + g * nnz_source * 32 + lane;
-  const double* xg = x + g * n * 32 + lane;
+  const double* rg = r + g * n * 32 + lane;
+  const double* bg = b + g * n * 32 + lane;
   double s0 = 0.0, s1 = 0.0;
-  for (int32_t i = i0; i < i1; ++i) {
-    double acc = 0.0;
-    for (int32_t k = __ldg(row_ptr + i); k < __ldg(row_ptr + i + 1); ++k) {
-      acc = add_prod(acc, ag[static_cast<int64_t>(k) * 32], xg[static_cast<int64_t>(__ldg(col + k)) * 32]);
+  int32_t i = i0;
+  for (; i + 8 <= i1; i += 8) {
+    double rv[8], bv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      rv[q] = rg[static_cast<int64_t>(i + q) * 32];
+      bv[q] = bg[static_cast<int64_t>(i + q) * 32];
     }
-    const double bi = b[(g * n + i) * 32 + lane];
-    const double ri = __dsub_rn(bi, acc);
-    r[(g * n + i) * 32 + lane] = ri;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s0 = add_prod(s0, rv[q], rv[q]);
+      s1 = add_prod(s1, bv[q], bv[q]);
+    }
+  }
+  for (; i < i1; ++i) {
+    const double ri = rg[static_cast<int64_t>(i) * 32], bi = bg[static_cast<int64_t>(i) * 32];
     s0 = add_prod(s0, ri, ri);
     s1 = add_prod(s1, bi, bi);
   }
@@ -882,11 +908,21 @@ bdot_kernel(int32_t n, const double* __restrict__ u, const double* __restrict__ 
   const int64_t g = blockIdx.y;
   int32_t i0, i1;
   brow_range(n, i0, i1);
+  const double* ug = u + g * n * 32 + lane;
+  const double* vg = v + g * n * 32 + lane;
   double s0 = 0.0;
-  for (int32_t i = i0; i < i1; ++i) {
-    const int64_t o = (g * n + i) * 32 + lane;
-    s0 = add_prod(s0, u[o], v[o]);
+  int32_t i = i0;
+  for (; i + 8 <= i1; i += 8) {  // 8 rows of loads in flight, the additions in row order
+    double uv[8], vv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uv[q] = ug[static_cast<int64_t>(i + q) * 32];
+      vv[q] = vg[static_cast<int64_t>(i + q) * 32];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s0 = add_prod(s0, uv[q], vv[q]);
   }
+  for (; i < i1; ++i) s0 = add_prod(s0, ug[static_cast<int64_t>(i) * 32], vg[static_cast<int64_t>(i) * 32]);
   const int64_t part = blockIdx.x * 8 + (threadIdx.x >> 5);
   partials[((g * 2 + 0) * kBatchParts + part) * 32 + lane] = s0;
 }
@@ -897,8 +933,16 @@ bfinish_kernel(int32_t count, int32_t padded, const double* __restrict__ partial
   const int lane = threadIdx.x;
   const int64_t g = blockIdx.x;
   for (int q = 0; q < count; ++q) {
+    const double* pp = partials + (g * 2 + q) * kBatchParts * 32 + lane;
     double s = 0.0;
-    for (int part = 0; part < kBatchParts; ++part) s += partials[((g * 2 + q) * kBatchParts + part) * 32 + lane];
+    static_assert(kBatchParts % 16 == 0, "unrolled fold");
+    for (int part = 0; part < kBatchParts; part += 16) {  // 16 loads in flight, folded in part order
+      double pv[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) pv[t] = pp[static_cast<int64_t>(part + t) * 32];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) s += pv[t];
+    }
     out[static_cast<int64_t>(q) * padded + g * 32 + lane] = s;
   }
 }
