@@ -531,7 +531,7 @@ b200lu_status b200lu_analyze(int64_t n64, const int64_t* row_offsets, const int6
   if (!out) return B200LU_INVALID_ARGUMENT;
   *out = nullptr;
   if (n64 < 0 || !row_offsets || (n64 > 0 && row_offsets[n64] > 0 && !col_indices)) return B200LU_INVALID_ARGUMENT;
-  if (n64 >= (int64_t{1} << 31) - 1 || row_offsets[n64] >= (int64_t{1} << 31)) return B200LU_INVALID_ARGUMENT;
+  if (n64 >= (int64_t{1} << 31) - 1 || row_offsets[n64] < 0 || row_offsets[n64] >= (int64_t{1} << 31)) return B200LU_INVALID_ARGUMENT;
   b200lu_analysis* a = new (std::nothrow) b200lu_analysis();
   if (!a) return B200LU_INVALID_ARGUMENT;
   *out = a;

@@ -23,6 +23,7 @@
 #include "schedule.hpp"
 #include "tile.cuh"
 #include "gather.cuh"
+#include "snode.cuh"
 
 using namespace b200lu;
 
@@ -105,6 +106,14 @@ struct b200lu_batch {
   void (*gather_fn)(BGatherArgs) = nullptr;
   int gather_grid = 0;
   size_t gather_smem = 0;
+  // supernodal trailing part (snode.cuh): dense runs of nested pivot rows, register accumulation per destination
+  bool use_snode = false;
+  SBlock* d_s_blocks = nullptr;
+  SRun* d_s_runs = nullptr;
+  uint32_t* d_s_dest = nullptr;
+  int32_t n_s_blocks = 0, snode_rows_per = 2;
+  void (*snode_fn)(BSnodeArgs) = nullptr;
+  int snode_grid = 0;
   RowMeta *d_lower_meta = nullptr, *d_upper_meta = nullptr;
   void* d_dest = nullptr;
   int32_t* d_src_of_slot = nullptr;
@@ -322,7 +331,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
         cnt, h->groups, h->nnz_factors, h->d_trivial_rows, h->d_diag, h->d_values, h->pivot_floor, h->d_failed);
     ST_TRY(check_launch(h, "btrivial_pivot_kernel"));
   }
-  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0 || h->n_tiles > 0 || h->n_g_blocks > 0) {
+  if (h->n_factor_rows > 0 || h->n_blocks > 0 || h->n_tail_rows > 0 || h->n_tiles > 0 || h->n_g_blocks > 0 || h->n_s_blocks > 0) {
     BFactorArgs a;
     a.n_rows = h->n_factor_rows;
     a.units = h->units;
@@ -355,6 +364,24 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       ta.ticket = h->d_tickets + 1;
       h->tile_fn<<<h->tile_grid, (h->tile_rows_per + 1) * 32, h->tile_smem, h->stream>>>(ta);
       ST_TRY(check_launch(h, "bfactor_tile_kernel"));
+    }
+    if (h->use_snode && h->n_s_blocks > 0) {
+      BSnodeArgs sa;
+      sa.n_blocks = h->n_s_blocks;
+      sa.units = h->units;
+      sa.gen = h->gen;
+      sa.blocks = h->d_s_blocks;
+      sa.runs = h->d_s_runs;
+      sa.dest = h->d_s_dest;
+      sa.diag = h->d_diag;
+      sa.values = h->d_values;
+      sa.nnz_factors = h->nnz_factors;
+      sa.flags = h->d_flags;
+      sa.pivot_floor = h->pivot_floor;
+      sa.failed = h->d_failed;
+      sa.ticket = h->d_tickets + 1;
+      h->snode_fn<<<h->snode_grid, 256, 0, h->stream>>>(sa);
+      ST_TRY(check_launch(h, "bfactor_snode_kernel"));
     }
     if (h->use_gather && h->n_g_blocks > 0) {
       BGatherArgs ga;
@@ -1154,6 +1181,50 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
       tail_rows.clear();
     }
+    //   * bfactor_snode_kernel (snode.cuh): 2-row blocks x 32 scenarios over RUNS of up to 8 consecutive pivot rows with
+    //     nested upper patterns (fundamental supernodes: 80 % of the update pairs at C2 sit in runs of >= 8 rows):
+    //     multipliers in registers, every destination entry loaded / stored once per run, no per-update index.
+    //     Bit-exact and free of L2 reductions, but it LOSES on this DAG: 58 ms (46 ms with single-row blocks) against
+    //     24.4 ms at C2 x 256, 33 / 19 ms against 8.2 (4.9 tiled) at 32 scenarios. ncu: the warps sit in the flag
+    //     waits — the trailing DAG is ~18 rows wide over 925 levels, a level costs what ONE warp needs to apply the
+    //     row's last pivots, and here that is ~15 dependent memory round trips (run record, diagonal slots, flag,
+    //     phase A per pivot, destination slots, phase B a few entries at a time, pivot check, fence) against ~4 for
+    //     the row-blocked kernel, whose reductions need no round trip for the destination at all. What it would take:
+    //     records / slots / destination values prefetched while the flag is awaited, the pivot rows streamed through a
+    //     shared-memory ring, L2 reductions for the single-pivot runs at the end of a row. Kept as an experiment, OFF.
+    // B200LU_BATCH_SNODE = 1 selects it; B200LU_SNODE_R (1, 2), B200LU_SNODE_SMALL: length of the shortest (last) runs.
+    e = std::getenv("B200LU_BATCH_SNODE");
+    const bool want_snode = e ? std::atoi(e) != 0 : false;
+    if (want_snode && !tail_rows.empty() && tail_mode != 0) {
+      e = std::getenv("B200LU_SNODE_SMALL");
+      const int ss = e ? std::atoi(e) : 1;
+      e = std::getenv("B200LU_SNODE_R");
+      int sr = e ? std::atoi(e) : 2;
+      SnodePlan plan;
+      std::string err;
+      if (!build_snode_plan(S.row_ptr, S.col, S.diag, S.lower_level, tail_rows, sr, ss, &plan, &err)) {
+        sr = 1;  // single-row blocks cannot depend on each other both ways
+        if (!build_snode_plan(S.row_ptr, S.col, S.diag, S.lower_level, tail_rows, sr, ss, &plan, &err)) {
+          h->last_error = err;
+          return B200LU_INVALID_ARGUMENT;
+        }
+      }
+      ST_TRY(dev_upload(h, &h->d_s_blocks, plan.blocks));
+      ST_TRY(dev_upload(h, &h->d_s_runs, plan.runs));
+      ST_TRY(dev_upload(h, &h->d_s_dest, plan.dest));
+      h->use_snode = true;
+      h->n_s_blocks = static_cast<int32_t>(plan.blocks.size());
+      h->snode_rows_per = sr;
+      if (std::getenv("B200LU_GATHER_VERBOSE")) {
+        std::fprintf(stderr, "snode plan: R %d rows %lld blocks %zu runs %zu pivots %lld (%.2f per run) pairs %lld (in runs >= 4: %.3f) dest entries %zu\n",
+                     sr, static_cast<long long>(plan.rows), plan.blocks.size(), plan.runs.size(), static_cast<long long>(plan.pivots),
+                     plan.runs.empty() ? 0.0 : static_cast<double>(plan.pivots) / plan.runs.size(), static_cast<long long>(plan.pairs),
+                     plan.pairs ? static_cast<double>(plan.pairs_in_runs_of_4) / plan.pairs : 0.0, plan.dest.size());
+      }
+      h->n_block_rows = static_cast<int32_t>(tail_rows.size());
+      for (int32_t i : tail_rows) h->blocked_pairs += S.pair_row_ptr[i + 1] - S.pair_row_ptr[i];
+      tail_rows.clear();
+    }
     std::vector<BlockMeta> blocks;
     std::vector<MergedPivot> merged;
     for (size_t b0 = 0; b0 < tail_rows.size(); b0 += kBlockRows) {
@@ -1363,6 +1434,17 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     int bocc = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, h->block_smem));
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
+    if (h->use_snode) {
+      using SFn = void (*)(BSnodeArgs);
+      const char* em = std::getenv("B200LU_SNODE_MINB");
+      const int minb = em ? std::atoi(em) : 2;
+      SFn sfn = h->snode_rows_per == 1 ? (minb >= 3 ? bfactor_snode_kernel<1, 3> : bfactor_snode_kernel<1, 2>)
+                                       : (minb >= 3 ? bfactor_snode_kernel<2, 3> : bfactor_snode_kernel<2, 2>);
+      h->snode_fn = sfn;
+      int socc = 0;
+      CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, sfn, 256, 0));
+      h->snode_grid = prop.multiProcessorCount * std::max(1, socc);
+    }
     if (h->use_gather) {
       using GFn = void (*)(BGatherArgs);
       const char* em = std::getenv("B200LU_GATHER_MINB");
@@ -1429,7 +1511,7 @@ void b200lu_batch_destroy(b200lu_batch* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_g_blocks, h->d_g_batches, h->d_g_recs, h->d_g_waits, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_tile_prof, h->d_lower_meta,
+  void* ptrs[] = {h->d_row_ptr, h->d_col, h->d_diag, h->d_trivial_rows, h->d_pair_row_ptr, h->d_factor_meta, h->d_tail_meta, h->d_blocks, h->d_merged, h->d_g_blocks, h->d_g_batches, h->d_g_recs, h->d_g_waits, h->d_s_blocks, h->d_s_runs, h->d_s_dest, h->d_tile_meta, h->d_tile_rows, h->d_tile_ext, h->d_tile_row_items, h->d_tile_dest, h->d_tile_flags, h->d_tile_prof, h->d_lower_meta,
                   h->d_upper_meta, h->d_dest, h->d_src_of_slot, h->d_scatter_scale, h->d_p, h->d_pq, h->d_row_scale,
                   h->d_col_scale, h->d_a_row_ptr, h->d_a_col, h->d_kkt_hdiag, h->d_kkt_dy, h->d_kkt_stage, h->d_kkt_pos, h->d_a_int, h->d_values, h->d_flags, h->d_failed, h->d_tickets,
                   h->d_stage_a, h->d_stage_in, h->d_stage_in2, h->d_stage_out, h->d_gather, h->d_w, h->d_t1, h->d_t2, h->d_b,
@@ -1812,7 +1894,7 @@ b200lu_status b200lu_batch_get_info(const b200lu_batch* h, b200lu_batch_info* ou
   out->unit_scenarios = h->unit;
   out->factor_rows = h->n_factor_rows + h->n_block_rows;
   out->blocked_rows = h->n_block_rows;
-  out->blocks = h->use_tiles ? h->n_tiles : h->use_gather ? h->n_g_blocks : h->n_blocks;
+  out->blocks = h->use_tiles ? h->n_tiles : h->use_snode ? h->n_s_blocks : h->use_gather ? h->n_g_blocks : h->n_blocks;
   out->blocked_pairs = h->blocked_pairs;
   out->factor_grid = h->factor_grid;
   out->tri_grid = h->tri_grid;

@@ -137,6 +137,36 @@ def test_batch_gather_form_is_bit_exact(rows, batch_len, small, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("rows,small", [(2, 1), (2, 2), (1, 1), (2, 0)])
+def test_batch_supernodal_form_is_bit_exact(rows, small, monkeypatch):
+    """The experimental supernodal form of the trailing refactorization (csrc/snode.cuh: runs of up to 8 consecutive pivot
+    rows with nested upper patterns, multipliers in registers, every destination entry loaded and stored once per run).
+    Off by default (slower than the default kernels on the narrow trailing DAG); bit-exact."""
+    monkeypatch.setenv("B200LU_BATCH_SNODE", "1")
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    monkeypatch.setenv("B200LU_SNODE_R", str(rows))
+    monkeypatch.setenv("B200LU_SNODE_SMALL", str(small))
+    fx = kkt_fixture(700, 300, num_systems=4)
+    f = BatchedFactors(fx.sym, 17)
+    info = f.info
+    f.close()
+    assert info["blocks"] > 0 and info["blocked_rows"] > 0 and not info["tiled"]
+    _check_batch(fx, 17, refine=False)
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+    # a banded matrix: every row of the band is one long supernode chain
+    n, band = 300, 12
+    M = np.zeros((n, n))
+    rng = np.random.default_rng(11)
+    for i in range(n):
+        lo, hi = max(0, i - band), min(n, i + band + 1)
+        M[i, lo:hi] = rng.uniform(-1, 1, hi - lo)
+        M[i, i] = 2.0 * band + 1.0
+    _check_batch(dense_fixture(M), 9, refine=False)
+
+
+@needs_ref
 def test_batch_long_pivot_rows_cross_chunks():
     """A banded matrix with 40 upper entries per row: every pivot row spans several load batches."""
     n, band = 400, 40
