@@ -22,6 +22,7 @@
 #include <queue>
 #include <set>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -136,17 +137,29 @@ constexpr i32 kDenseDegrees = 96;
 // queue is one ordered vertex set per degree (below).
 std::vector<i32> amd_order_fast(const Csr32& S) {
   const i32 n = S.n;
-  std::vector<std::vector<i32>> var_adj(n), elem_adj(n), elem_vars(n);
-  std::vector<char> eliminated(n, 0), elem_alive(n, 0);
-  std::vector<i32> degree(n, 0);
+  // Flat storage, laid out for the two inner loops (which are cache-miss bound): the variable neighbours of a vertex are
+  // a slice of one array that only ever shrinks in place; its adjacent elements are a short inline list (overflow into a
+  // side vector); everything the degree arithmetic reads about an element sits in one 16-byte record.
+  struct Elem {
+    i32 stamp, external, size, alive;
+  };
+  constexpr int kInline = 6;
+  std::vector<i64> var_beg(n);
+  std::vector<i32> var_len(n), var_pool, degree(n, 0), elen(n, 0), einl(static_cast<size_t>(n) * kInline);
+  std::vector<std::vector<i32>> eover(n);  // elements beyond the inline capacity (rare)
+  std::vector<std::vector<i32>> elem_vars(n);
+  std::vector<Elem> einfo(n, Elem{-1, 0, 0, 0});
+  std::vector<char> eliminated(n, 0);
+  var_pool.reserve(S.col.size());
   for (i32 i = 0; i < n; ++i) {
-    auto& a = var_adj[i];
-    a.reserve(S.ptr[i + 1] - S.ptr[i]);
+    var_beg[i] = static_cast<i64>(var_pool.size());
     for (i64 k = S.ptr[i]; k < S.ptr[i + 1]; ++k) {
-      if (S.col[k] != i) a.push_back(S.col[k]);
+      if (S.col[k] != i) var_pool.push_back(S.col[k]);
     }
-    degree[i] = static_cast<i32>(a.size());
+    var_len[i] = static_cast<i32>(static_cast<i64>(var_pool.size()) - var_beg[i]);
+    degree[i] = var_len[i];
   }
+  auto elem_at = [&](i32 i, i32 q) -> i32& { return q < kInline ? einl[static_cast<size_t>(i) * kInline + q] : eover[i][q - kInline]; };
   // Pivot queue: one ordered vertex set per degree value — a hierarchical bitmap (64-ary, find-first by
   // count-trailing-zeros) for the small degrees almost every vertex has, std::set for the rare large ones.
   // Exact membership (erase old degree, insert new), so the minimum (degree, vertex) costs a handful of words.
@@ -170,7 +183,7 @@ std::vector<i32> amd_order_fast(const Csr32& S) {
   };
   for (i32 i = 0; i < n; ++i) insert(degree[i], i);
   i32 mindeg = 0;
-  std::vector<i32> mark(n, -1), elem_stamp(n, -1), elem_external(n, 0), pivot_set, order(n);
+  std::vector<i32> mark(n, -1), pivot_set, order(n);
   for (i32 step = 0; step < n; ++step) {
     i32 p;
     while (true) {  // every vertex alive is in exactly one set, so this terminates
@@ -186,65 +199,71 @@ std::vector<i32> amd_order_fast(const Csr32& S) {
     erase(mindeg, p);
     order[step] = p;
     eliminated[p] = 1;
+    // L_p = (A_p ∪ spans of the adjacent elements) \ {p}
     pivot_set.clear();
     mark[p] = step;
-    for (i32 v : var_adj[p]) {
+    for (i32 q = 0; q < var_len[p]; ++q) {
+      const i32 v = var_pool[var_beg[p] + q];
       if (!eliminated[v] && mark[v] != step) {
         mark[v] = step;
         pivot_set.push_back(v);
       }
     }
-    for (i32 e : elem_adj[p]) {
+    for (i32 q = 0; q < elen[p]; ++q) {
+      const i32 e = elem_at(p, q);
       for (i32 v : elem_vars[e]) {
         if (mark[v] != step) {
           mark[v] = step;
           pivot_set.push_back(v);
         }
       }
+      einfo[e].alive = 0;  // absorbed; its span is never read again
     }
-    for (i32 e : elem_adj[p]) {
-      elem_alive[e] = 0;
-      std::vector<i32>().swap(elem_vars[e]);
-    }
-    std::vector<i32>().swap(var_adj[p]);
-    std::vector<i32>().swap(elem_adj[p]);
-    elem_vars[p] = pivot_set;  // (the reference sorts the span; nothing below depends on its order)
-    elem_alive[p] = 1;
+    var_len[p] = 0;
+    elen[p] = 0;
+    elem_vars[p].assign(pivot_set.begin(), pivot_set.end());  // (the reference sorts the span; nothing below depends on its order)
+    einfo[p].alive = 1;
+    einfo[p].size = static_cast<i32>(pivot_set.size());
 
+    // |L_e \ L_p| for every live element touching L_p
     for (i32 i : pivot_set) {
-      for (i32 e : elem_adj[i]) {
-        if (!elem_alive[e] || e == p) continue;
-        if (elem_stamp[e] != step) {
-          elem_stamp[e] = step;
-          elem_external[e] = static_cast<i32>(elem_vars[e].size());
+      for (i32 q = 0; q < elen[i]; ++q) {
+        Elem& E = einfo[elem_at(i, q)];
+        if (!E.alive) continue;
+        if (E.stamp != step) {
+          E.stamp = step;
+          E.external = E.size;
         }
-        elem_external[e]--;
+        E.external--;
       }
     }
     const i32 alive_after = n - step - 1;
     const i32 lp_minus_self = static_cast<i32>(pivot_set.size()) - 1;
     const i32 bound_world = std::max<i32>(alive_after - 1, 0);
     for (i32 i : pivot_set) {
-      auto& av = var_adj[i];
-      size_t w = 0;
-      for (size_t r = 0; r < av.size(); ++r) {
+      i32* av = var_pool.data() + var_beg[i];
+      i32 w = 0;
+      for (i32 r = 0; r < var_len[i]; ++r) {
         const i32 v = av[r];
         if (!(v == p || mark[v] == step)) av[w++] = v;
       }
-      av.resize(w);
-      auto& ae = elem_adj[i];
-      w = 0;
+      var_len[i] = w;
+      i32 we = 0;
       i64 external_sum = 0;
-      for (size_t r = 0; r < ae.size(); ++r) {
-        const i32 e = ae[r];
-        if (!elem_alive[e]) continue;
-        ae[w++] = e;
-        external_sum += (elem_stamp[e] == step) ? elem_external[e] : static_cast<i32>(elem_vars[e].size());
+      for (i32 r = 0; r < elen[i]; ++r) {
+        const i32 e = elem_at(i, r);
+        const Elem& E = einfo[e];
+        if (!E.alive) continue;
+        elem_at(i, we++) = e;
+        external_sum += (E.stamp == step) ? E.external : E.size;
       }
-      ae.resize(w);
-      ae.push_back(p);
+      if (we >= kInline) {
+        if (static_cast<i32>(eover[i].size()) < we - kInline + 1) eover[i].resize(static_cast<size_t>(we - kInline + 1));
+      }
+      elem_at(i, we++) = p;
+      elen[i] = we;
       const i64 bound_prev = static_cast<i64>(degree[i]) + lp_minus_self;
-      const i64 bound_sets = static_cast<i64>(av.size()) + lp_minus_self + external_sum;
+      const i64 bound_sets = static_cast<i64>(w) + lp_minus_self + external_sum;
       const i32 nd = static_cast<i32>(std::min<i64>({bound_world, bound_prev, bound_sets}));
       if (nd != degree[i]) {
         erase(degree[i], i);
@@ -613,15 +632,34 @@ b200lu_status b200lu_analyze(int64_t n64, const int64_t* row_offsets, const int6
   // scatter map and scale (src/symbolic.cpp:182-201)
   a->scatter_map.resize(nnz);
   a->scatter_scale.assign(nnz, 1.0);
-  for (i32 i = 0; i < n; ++i) {
-    const i32 r = amd[i];
-    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-      const i32 j = A.col[k];
-      const i32 c = amd[use_scaling ? colperm[j] : j];
-      const i64 slot = find_entry(F.ptr.data(), F.col.data(), r, c);
-      if (slot < 0) return fail(B200LU_INVALID_ARGUMENT, "combined pattern must contain every source entry");
-      a->scatter_map[k] = slot;
-      if (use_scaling) a->scatter_scale[k] = a->row_scale[i] * a->col_scale[j];
+  {
+    // rows are independent: split over host threads (the only multi-threaded stage; the result does not depend on it)
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = nnz < (i64{1} << 18) ? 1u : hw;
+    std::vector<char> bad(nt, 0);
+    auto work = [&](unsigned t) {
+      const i32 lo = static_cast<i32>(static_cast<i64>(n) * t / nt), hi = static_cast<i32>(static_cast<i64>(n) * (t + 1) / nt);
+      for (i32 i = lo; i < hi; ++i) {
+        const i32 r = amd[i];
+        for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+          const i32 j = A.col[k];
+          const i32 c = amd[use_scaling ? colperm[j] : j];
+          const i64 slot = find_entry(F.ptr.data(), F.col.data(), r, c);
+          if (slot < 0) bad[t] = 1;
+          a->scatter_map[k] = slot;
+          if (use_scaling) a->scatter_scale[k] = a->row_scale[i] * a->col_scale[j];
+        }
+      }
+    };
+    if (nt == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (unsigned t = 0; t < nt; ++t) pool.emplace_back(work, t);
+      for (auto& th : pool) th.join();
+    }
+    for (char b : bad) {
+      if (b) return fail(B200LU_INVALID_ARGUMENT, "combined pattern must contain every source entry");
     }
   }
   a->row_offsets = std::move(F.ptr);
