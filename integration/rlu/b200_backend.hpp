@@ -42,7 +42,7 @@ inline b200lu_symbolic_view view_of(const SymbolicFactors& s) {
 }
 
 // symbolic_analyze (symbolic.hpp:72-75, src/symbolic.cpp:156-203) through b200lu_analyze: the same SymbolicFactors —
-// permutations, scale factors, combined pattern, diag_pos, scatter map — bit for bit, 3-16x sooner (host code only; no
+// permutations, scale factors, combined pattern, diag_pos, scatter map — bit for bit, 4-20x sooner (host code only; no
 // device involved). `row_lookup`, the CPU elimination's per-row hash / bitmap, is built only when asked for: the device
 // path never reads it, the reference's own factorize / refactorize do.
 inline SymbolicFactors symbolic_analyze(const CsrMatrix& A, const AnalyzeOptions& options = {}, bool with_row_lookup = false) {
