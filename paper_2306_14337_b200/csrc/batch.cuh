@@ -418,7 +418,7 @@ struct BBlockArgs {
 #define B200LU_BLOCK_STAGE 48
 #endif
 constexpr int kBlockStage = B200LU_BLOCK_STAGE;
-constexpr int kBlockStageDest = 32;  // doubles reserved per row for its destination slice (256 bytes)
+constexpr int kBlockStageDest = kBlockStage * 4 + 8 <= 256 ? 32 : (kBlockStage * 4 + 8 + 7) / 8;  // doubles reserved per row for its destination slice (256 bytes at the default stage)
 __host__ __device__ constexpr size_t block_stage_doubles() {
   return kBlockStage > 0 ? static_cast<size_t>(kBlockStage) * 32 + kBlockRows * kBlockStageDest : 0;
 }
