@@ -664,7 +664,11 @@ def run_batch(args):
                 "unit_scenarios": info["unit_scenarios"], "device_gb": round(info["device_bytes"] / 1e9, 2),
                 "l2": "256 MiB device buffer zeroed between timed steps (outside the per-step event pair); the "
                       "per-step working set (9 GB of factor values at 256 scenarios) exceeds the 126 MB L2 anyway",
-                "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks",
+                "timing": "per-step CUDA events on the launching stream, summed over steps; max over ranks. `value` goes "
+                          "through the plain calls, each of which ends with a host read-back (failed rows, norms): those "
+                          "synchronisation gaps (1-3 ms per step, host dependent) are inside `value`; `e2e` runs K steps "
+                          "through the staged calls under one event pair, where nothing waits for the host — which is why it "
+                          "can come out above `value` although it also moves the data over PCIe",
             },
             "clocks": clocks,
             "ms_per_system": ms_per_step / total_scen,
