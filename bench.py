@@ -350,6 +350,33 @@ def measure_single(args, workload, steps, with_cpu_baseline):
     st = f.stats
     f.close()
 
+    # ---- the same step with B200LU_FLAG_STRICT_ORDER: both sweeps fold in the reference's ascending column order, so
+    # solve_system is bit-identical to the CPU result (the path the bitwise parity tests run); the default above folds
+    # U rows in production order and is checked on the residual. Reported beside it, never as the headline.
+    strict = None
+    if not args.no_refine:
+        fs = rlu.NumericFactors(sym, rlu.FactorOptions(device=local_rank, stream=stream.cuda_stream, strict_order=True))
+
+        def step_strict(k):
+            rlu.refactorize(fs, dev_mats[k])
+            x = rlu.solve_system(fs, dev_rhs[k])
+            return rlu.fgmres_refine(fs, dev_rhs[k], x, cfg)
+        for w in range(3):
+            step_strict(w % nsys)
+        torch.cuda.synchronize()
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for s_ in range(steps):
+            flush.zero_()
+            sev[s_][0].record()
+            out_s = step_strict(s_ % nsys)
+            sev[s_][1].record()
+        torch.cuda.synchronize()
+        strict = {"ms_per_step": sum(a.elapsed_time(b) for a, b in sev) / steps,
+                  "relres_final": float(seq.matrix((steps - 1) % nsys).relative_residual(out_s.x.cpu().numpy(), seq.rhs((steps - 1) % nsys))),
+                  "note": "same step on a handle created with strict_order (B200LU_FLAG_STRICT_ORDER): lower/upper/solve_system "
+                          "bit-identical to the reference (tests/test_gpu_parity.py, test_gpu_fullsize.py)"}
+        fs.close()
+
     # ---- max over ranks
     t = torch.tensor([total_ms, e2e_total_ms, relres], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -389,6 +416,7 @@ def measure_single(args, workload, steps, with_cpu_baseline):
                         "the public refactorize/solve_system/fgmres_refine calls"},
         "gpu_launches": launches,
         "analysis": analysis,
+        "strict_order": strict,
         "phases_ms_per_step": {p: v[0] / steps for p, v in phases.items()},
         "launches_per_step": {p: v[1] / steps for p, v in phases.items()},
         "refine_iters_median": med_iters, "relres_final_max": relres_max,
@@ -722,6 +750,7 @@ def run_batch(args):
         if single is not None:
             line["single_system"] = {k: single[k] for k in keys}
             line["single_system"]["analysis"] = single.get("analysis")
+            line["single_system"]["strict_order"] = single.get("strict_order")
         if c4 is not None:
             line["c4"] = {k: c4[k] for k in keys}
             line["c4"]["analysis"] = c4.get("analysis")
