@@ -1434,6 +1434,12 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     int bocc = 0;
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, 256, h->block_smem));
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
+    // experiment: fewer resident CTAs (a smaller working set in L2). Measured at C2 x 256, factor phase: 296 CTAs 24.3 ms,
+    // 222: 26.7, 148: 29.9, 111: 36.1, 74: 49.9 (at 32 scenarios 8.2 / 8.3 / 8.4 / 9.1 / 10.9): residency pays, L2 locality does not.
+    if (const char* eg = std::getenv("B200LU_BLOCK_GRID")) {
+      const int want = std::atoi(eg);
+      if (want > 0) h->block_grid = std::min(h->block_grid, want);
+    }
     if (h->use_snode) {
       using SFn = void (*)(BSnodeArgs);
       const char* em = std::getenv("B200LU_SNODE_MINB");
