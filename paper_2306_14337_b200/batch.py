@@ -117,6 +117,13 @@ def _symbolic_view(sym: rlu.SymbolicFactors):
     return v
 
 
+_OUTCOME_DTYPE = np.dtype({"names": ["iterations", "converged", "history_len", "residual_history"],
+                           "formats": [np.int32, np.int32, np.int32, (np.float64, 66)],
+                           "offsets": [_capi.RefineOutcome.iterations.offset, _capi.RefineOutcome.converged.offset,
+                                       _capi.RefineOutcome.history_len.offset, _capi.RefineOutcome.residual_history.offset],
+                           "itemsize": C.sizeof(_capi.RefineOutcome)})
+
+
 class BatchedFactors:
     """`batch` NumericFactors (include/rlu/numeric.hpp:22-31) over one SymbolicFactors, stored
     scenario-interleaved on the device. Value arrays are [batch, nnz(A)], vectors [batch, n]
@@ -300,9 +307,16 @@ class BatchedFactors:
         ocs = (_capi.RefineOutcome * self.batch)()
         self._check(getattr(_capi.lib(), fn_name)(self._h, pb, px, po, dev, 1 if preconditioned else 0,
                                                   C.byref(cfg), C.cast(ocs, C.c_void_p)))
-        outcomes = [rlu.RefineOutcome(out[s], int(o.iterations), list(o.residual_history[:o.history_len]),
-                                      bool(o.converged)) for s, o in enumerate(ocs)]
-        return out, outcomes
+        return out, self._outcomes(ocs, out)
+
+    def _outcomes(self, ocs, out):
+        """RefineOutcome per scenario from the C records: one numpy view of the records instead of 256 x (tensor
+        indexing + ctypes field reads) — at C2 x 256 those per-scenario Python objects cost more host time than the
+        three read-backs of the refinement itself."""
+        rec = np.frombuffer(ocs, dtype=_OUTCOME_DTYPE, count=self.batch)
+        its, conv, hl, hist = rec["iterations"].tolist(), rec["converged"].tolist(), rec["history_len"].tolist(), rec["residual_history"]
+        xs = out.unbind(0) if hasattr(out, "unbind") else out
+        return [rlu.RefineOutcome(xs[s], its[s], hist[s, :hl[s]].tolist(), bool(conv[s])) for s in range(self.batch)]
 
     # -- staged (pipelined) submission ------------------------------------------
     def _host_ptr(self, a, width, what):
@@ -352,8 +366,7 @@ class BatchedFactors:
                                                                  C.cast(ocs, C.c_void_p), failed.ctypes.data), failed)
         if not refine:
             return []
-        return [rlu.RefineOutcome(out[s], int(o.iterations), list(o.residual_history[:o.history_len]), bool(o.converged))
-                for s, o in enumerate(ocs)]
+        return self._outcomes(ocs, out if not isinstance(out, np.ndarray) or out.ndim == 2 else out.reshape(self.batch, -1))
 
     def staged_wait(self):
         self._check(_capi.lib().b200lu_batch_staged_wait(self._h))
