@@ -1501,6 +1501,13 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     h->tri_grid = prop.multiProcessorCount * std::max(1, o1);
     h->tri_grid_upper = prop.multiProcessorCount * std::max(1, o2);
     h->tri_grid_chain = prop.multiProcessorCount * std::max(1, o3);
+    // experiment: fewer resident CTAs in the U sweep. Measured at C2 x 256 (two sweeps per step): 444 CTAs 4.53 ms, 296: 5.76,
+    // 148: 9.40 (32 scenarios: 2.37 / 2.43 / 2.93) — the sweep is bound by how many rows are in flight, and those by the
+    // 16 KB parking buffer per warp; 28 % of the rows (76 % of the entries) have more than 33 upper entries, so a split
+    // into short-row and long-row CTAs would buy ~1.2x at best.
+    if (const char* eg = std::getenv("B200LU_BATCH_UGRID")) {
+      if (std::atoi(eg) > 0) h->tri_grid_chain = std::min(h->tri_grid_chain, std::atoi(eg));
+    }
     // chain part of the U sweep: the leading levels up to the first one at least kChainWidth rows wide
     const char* e = std::getenv("B200LU_BATCH_CHAIN_WIDTH");
     const int64_t chain_width = e ? std::atoll(e) : 512;
