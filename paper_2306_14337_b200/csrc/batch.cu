@@ -24,6 +24,7 @@
 #include "tile.cuh"
 #include "gather.cuh"
 #include "snode.cuh"
+#include "blockmc.cuh"
 
 using namespace b200lu;
 
@@ -78,6 +79,10 @@ struct b200lu_batch {
   void (*block_fn)(BBlockArgs) = nullptr;
   int block_grid = 0;
   size_t block_smem = 0;
+  int mc_contexts = 0;  // > 0: bfactor_block_mc_kernel with that many block contexts per warp (blockmc.cuh)
+  void (*mc_fn)(BBlockArgs, int) = nullptr;
+  int mc_grid = 0;
+  size_t mc_smem = 0;
   // tiled trailing part (tile.cuh): rows resident in shared memory, pivot rows streamed by TMA
   bool use_tiles = false, tile_auto = true;
 
@@ -422,8 +427,13 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       bb.pivot_floor = h->pivot_floor;
       bb.failed = h->d_failed;
       bb.ticket = h->d_tickets + 1;
-      h->block_fn<<<h->block_grid, 256, h->block_smem, h->stream>>>(bb);
-      ST_TRY(check_launch(h, "bfactor_block_kernel"));
+      if (h->mc_contexts > 0) {
+        h->mc_fn<<<h->mc_grid, 256, h->mc_smem, h->stream>>>(bb, h->mc_contexts);
+        ST_TRY(check_launch(h, "bfactor_block_mc_kernel"));
+      } else {
+        h->block_fn<<<h->block_grid, 256, h->block_smem, h->stream>>>(bb);
+        ST_TRY(check_launch(h, "bfactor_block_kernel"));
+      }
     }
   }
   CU_TRY(h, cudaMemcpyAsync(h->h_failed, h->d_failed, static_cast<size_t>(h->padded) * sizeof(int32_t),
@@ -1436,6 +1446,20 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
     // experiment: fewer resident CTAs (a smaller working set in L2). Measured at C2 x 256, factor phase: 296 CTAs 24.3 ms,
     // 222: 26.7, 148: 29.9, 111: 36.1, 74: 49.9 (at 32 scenarios 8.2 / 8.3 / 8.4 / 9.1 / 10.9): residency pays, L2 locality does not.
+    if (const char* emc = std::getenv("B200LU_BATCH_MC")) {
+      const int w = std::atoi(emc);
+      if (w >= 2 && w <= kMcMaxContexts) {
+        using MFn = void (*)(BBlockArgs, int);
+        MFn mfn = h->dest16 ? bfactor_block_mc_kernel<uint16_t, 2> : bfactor_block_mc_kernel<uint32_t, 2>;
+        h->mc_contexts = w;
+        h->mc_fn = mfn;
+        h->mc_smem = mc_smem_bytes(w);
+        CU_TRY(h, cudaFuncSetAttribute(mfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mc_smem_bytes(kMcMaxContexts))));
+        int mocc = 0;
+        CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, mfn, 256, h->mc_smem));
+        h->mc_grid = prop.multiProcessorCount * std::max(1, mocc);
+      }
+    }
     if (const char* eg = std::getenv("B200LU_BLOCK_GRID")) {
       const int want = std::atoi(eg);
       if (want > 0) h->block_grid = std::min(h->block_grid, want);

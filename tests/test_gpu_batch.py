@@ -167,6 +167,20 @@ def test_batch_supernodal_form_is_bit_exact(rows, small, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("contexts", [2, 4, 8])
+def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
+    """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
+    a context is left at the first pivot whose flag is not set instead of waited on). Off by default (slower)."""
+    monkeypatch.setenv("B200LU_BATCH_MC", str(contexts))
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    fx = kkt_fixture(700, 300, num_systems=4)
+    _check_batch(fx, 17, refine=False)
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+
+
+@needs_ref
 def test_batch_long_pivot_rows_cross_chunks():
     """A banded matrix with 40 upper entries per row: every pivot row spans several load batches."""
     n, band = 400, 40
