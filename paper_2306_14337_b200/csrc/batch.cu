@@ -25,6 +25,7 @@
 #include "gather.cuh"
 #include "snode.cuh"
 #include "blockmc.cuh"
+#include "blockteam.cuh"
 
 using namespace b200lu;
 
@@ -79,6 +80,8 @@ struct b200lu_batch {
   void (*block_fn)(BBlockArgs) = nullptr;
   int block_grid = 0;
   size_t block_smem = 0;
+  void (*team_fn)(BBlockArgs) = nullptr;  // bfactor_block_team_kernel (blockteam.cuh): two warps per block
+  int team_grid = 0;
   int mc_contexts = 0;  // > 0: bfactor_block_mc_kernel with that many block contexts per warp (blockmc.cuh)
   void (*mc_fn)(BBlockArgs, int) = nullptr;
   int mc_grid = 0;
@@ -427,7 +430,10 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       bb.pivot_floor = h->pivot_floor;
       bb.failed = h->d_failed;
       bb.ticket = h->d_tickets + 1;
-      if (h->mc_contexts > 0) {
+      if (h->team_fn) {
+        h->team_fn<<<h->team_grid, kTeamWarps * 32, team_smem_bytes(), h->stream>>>(bb);
+        ST_TRY(check_launch(h, "bfactor_block_team_kernel"));
+      } else if (h->mc_contexts > 0) {
         h->mc_fn<<<h->mc_grid, 256, h->mc_smem, h->stream>>>(bb, h->mc_contexts);
         ST_TRY(check_launch(h, "bfactor_block_mc_kernel"));
       } else {
@@ -1446,6 +1452,23 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     h->block_grid = prop.multiProcessorCount * std::max(1, bocc);
     // experiment: fewer resident CTAs (a smaller working set in L2). Measured at C2 x 256, factor phase: 296 CTAs 24.3 ms,
     // 222: 26.7, 148: 29.9, 111: 36.1, 74: 49.9 (at 32 scenarios 8.2 / 8.3 / 8.4 / 9.1 / 10.9): residency pays, L2 locality does not.
+    {
+      // Default for the row-blocked trailing part since round 2: one warp per ROW of a block (blockteam.cuh), the pivot row
+      // staged once per block. Measured at C2, factor phase: 22.3 ms against 24.4 ms at 256 scenarios, 5.9 ms against 8.2 ms
+      // at 32. B200LU_BATCH_TEAM = 0 restores bfactor_block_kernel (one warp per block); 2 / 3 / 4 = minimum CTAs per SM.
+      const char* et = std::getenv("B200LU_BATCH_TEAM");
+      const int minb = et ? std::atoi(et) : 3;
+      if (minb >= 1) {
+        using TFn = void (*)(BBlockArgs);
+        TFn tfn = h->dest16 ? (minb >= 4 ? bfactor_block_team_kernel<uint16_t, 4> : minb == 3 ? bfactor_block_team_kernel<uint16_t, 3> : bfactor_block_team_kernel<uint16_t, 2>)
+                            : bfactor_block_team_kernel<uint32_t, 2>;
+        h->team_fn = tfn;
+        CU_TRY(h, cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(team_smem_bytes())));
+        int tocc = 0;
+        CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tfn, kTeamWarps * 32, team_smem_bytes()));
+        h->team_grid = prop.multiProcessorCount * std::max(1, tocc);
+      }
+    }
     if (const char* emc = std::getenv("B200LU_BATCH_MC")) {
       const int w = std::atoi(emc);
       if (w >= 2 && w <= kMcMaxContexts) {

@@ -1,0 +1,145 @@
+// K2 batched, row-blocked trailing part with ONE WARP PER ROW OF A BLOCK (B200LU_BATCH_TEAM=minimum CTAs per SM).
+//
+// bfactor_block_kernel (batch.cuh) gives one warp both rows of a block: 126 registers and a 12.5 KB pivot-row stage
+// per warp, 16 warps per SM — and the resident-CTA sweep shows the launch is bound by how many warps execute side by
+// side (296 CTAs 24.3 ms, 148 CTAs 29.9 ms). Here a TEAM of two warps owns the block, one row each: the pivot row is
+// staged once per team (by member 0) and applied by each member to its own row, so the registers per warp are those of
+// a single row and the stage per warp is halved, at the DRAM / L2 traffic of 2-row blocks. Every row is still updated
+// by one thread per scenario, pivots ascending, reductions in program order: bit-exact for the same reason as
+// bfactor_block_kernel. The members meet at a named barrier twice per pivot (stage filled / stage free).
+#pragma once
+
+#include "batch.cuh"
+
+namespace b200lu {
+
+constexpr int kTeamWarps = 8;                        // warps per CTA
+constexpr int kTeamSize = kBlockRows;                // warps per team = rows per block (2, or 4 with -DB200LU_BLOCK_ROWS=4)
+constexpr int kTeams = kTeamWarps / kTeamSize;       // teams per CTA
+__host__ __device__ constexpr size_t team_stage_doubles() { return static_cast<size_t>(kBlockStage) * 32 + kTeamSize * kBlockStageDest; }
+__host__ __device__ constexpr size_t team_smem_bytes() { return kTeams * (team_stage_doubles() * sizeof(double) + 16); }
+
+__device__ __forceinline__ void team_barrier(int team) {
+  asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(32 * kTeamSize) : "memory");
+}
+
+template <typename DestT, int MINB>
+__global__ void __launch_bounds__(kTeamWarps * 32, MINB)
+bfactor_block_team_kernel(const BBlockArgs a) {
+  static_assert(kBlockStage > 0, "the team variant stages the pivot rows");
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int team = warp / kTeamSize, me = warp % kTeamSize;  // `me` = the block row this warp owns
+  const DestT* __restrict__ dest = static_cast<const DestT*>(a.dest);
+  extern __shared__ __align__(16) double team_smem[];
+  double* stage = team_smem + static_cast<size_t>(team) * team_stage_doubles();
+  unsigned long long* tslot = reinterpret_cast<unsigned long long*>(team_smem + kTeams * team_stage_doubles()) + team * 2;
+  const unsigned long long total = static_cast<unsigned long long>(a.n_blocks) * a.units_here;
+  while (true) {
+    if (me == 0 && lane == 0) *tslot = atomicAdd(a.ticket, 1ull);
+    team_barrier(team);
+    const unsigned long long t = *tslot;
+    team_barrier(team);  // both members have read the slot before the next claim overwrites it
+    if (t >= total) break;
+    const int32_t b = static_cast<int32_t>(t / a.units_here);
+    const int32_t u = a.first_unit + static_cast<int32_t>(t - static_cast<unsigned long long>(b) * a.units_here);
+    const int4 b0 = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
+    const int4 b1 = __ldg(reinterpret_cast<const int4*>(a.blocks + b) + 1);
+    const int32_t rows4[4] = {b0.x, b0.y, b0.z, b0.w};
+    const int32_t myrow = rows4[me];  // -1: the block is short of rows (this member just keeps step)
+    const int32_t mbeg = b1.x, mend = b1.y;
+    const int32_t sc0 = u * 32;
+    double* gbase = a.values + static_cast<int64_t>(u) * a.nnz_factors * 32 + lane;
+    const int32_t irow = max(myrow, 0);
+    const int32_t lo = __ldg(a.row_ptr + irow);
+    double* rowg = gbase + static_cast<int64_t>(lo) * 32;
+    const int32_t nl = __ldg(a.diag + irow) - lo;
+    int64_t p = a.pair_row_ptr[irow];
+    int32_t k = 0;
+    const uint32_t mybit = myrow >= 0 ? (1u << me) : 0u;
+
+    for (int32_t t0 = mbeg; t0 < mend; t0 += 32) {
+      int32_t my_d = 0, my_dd = 0, my_m = 0, my_ready = 0;
+      uint32_t my_bits = 0;
+      if (t0 + lane < mend) {
+        const int2 mp = __ldg(reinterpret_cast<const int2*>(a.merged) + t0 + lane);
+        my_d = mp.x;
+        my_bits = static_cast<uint32_t>(mp.y);
+        my_dd = __ldg(a.diag + my_d);
+        my_m = __ldg(a.row_ptr + my_d + 1) - my_dd - 1;
+        if (me == 0) my_ready = ld_acquire_s32(a.flags + static_cast<int64_t>(my_d) * a.units + u) >= a.gen;
+      }
+      __syncwarp();
+      const int32_t cnt = min(32, mend - t0);
+      for (int32_t q = 0; q < cnt; ++q) {
+        const int32_t dd = __shfl_sync(full, my_dd, q);
+        const int32_t m = __shfl_sync(full, my_m, q);
+        const uint32_t bits = __shfl_sync(full, my_bits, q);
+        const bool mine = (bits & mybit) != 0;
+        const double* ug = gbase + static_cast<int64_t>(dd) * 32;
+        const int32_t ns = min(m + 1, kBlockStage);  // staged entries of the pivot row (diagonal included)
+        // member 0 awaits the pivot row's flag and stages it for the team; each member stages its own destination slice
+        if (me == 0) {
+          if (!__shfl_sync(full, my_ready, q)) {
+            const int32_t d = __shfl_sync(full, my_d, q);
+            wait_flag(a.flags + static_cast<int64_t>(d) * a.units + u, a.gen);
+          }
+          __syncwarp();
+          const double* src = ug - lane;
+          for (int32_t t16 = lane; t16 < ns * 16; t16 += 32) cp_async_16(stage + t16 * 2, src + t16 * 2);
+        }
+        if (mine) {
+          const char* dsrc = reinterpret_cast<const char*>(dest + p);
+          const int32_t shift = static_cast<int32_t>(reinterpret_cast<uintptr_t>(dsrc) & 3);
+          const int32_t words = (static_cast<int32_t>((ns - 1) * sizeof(DestT)) + shift + 3) >> 2;
+          uint32_t* ddst = reinterpret_cast<uint32_t*>(stage + kBlockStage * 32 + me * kBlockStageDest);
+          for (int32_t t4 = lane; t4 < words; t4 += 32) cp_async_4(ddst + t4, dsrc - shift + 4 * t4);
+        }
+        // a_id is read while the copies are in flight (every earlier reduction to it was issued by this thread)
+        double nalpha = 0.0;
+        if (mine) nalpha = ld_cg(rowg + static_cast<int64_t>(k) * 32);
+        cp_async_commit_wait_all();
+        team_barrier(team);  // the stage is filled (and member 0 has acquired the pivot row's flag for both)
+        if (mine) {
+          const double udd = stage[lane];
+          nalpha = -(nalpha / udd);  // src/numeric.cpp:40; the sign is exact
+          const char* dbytes = reinterpret_cast<const char*>(stage + kBlockStage * 32 + me * kBlockStageDest);
+          const DestT* dl = reinterpret_cast<const DestT*>(dbytes + (reinterpret_cast<uintptr_t>(dest + p) & 3));
+#pragma unroll 4
+          for (int32_t cs = 0; cs < ns - 1; ++cs) {
+            red_add_f64(rowg + static_cast<int64_t>(dl[cs]) * 32, __dmul_rn(nalpha, stage[(1 + cs) * 32 + lane]));  // src/numeric.cpp:44
+          }
+          int32_t cc = ns - 1;
+          for (; cc + 7 < m; cc += 8) {  // the part of a long pivot row that did not fit the stage
+            double uv[8];
+            int32_t ds[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) uv[j] = ld_cg(ug + static_cast<int64_t>(1 + cc + j) * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ds[j] = dest[p + cc + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red_add_f64(rowg + static_cast<int64_t>(ds[j]) * 32, __dmul_rn(nalpha, uv[j]));
+          }
+          for (; cc < m; ++cc) {
+            const double uv = ld_cg(ug + static_cast<int64_t>(1 + cc) * 32);
+            red_add_f64(rowg + static_cast<int64_t>(dest[p + cc]) * 32, __dmul_rn(nalpha, uv));
+          }
+          st_cg(rowg + static_cast<int64_t>(k) * 32, -nalpha);  // l_id, src/numeric.cpp:41
+          p += m;
+          ++k;
+          if (bits & (256u << me)) {  // this row's last pivot: pivot check (src/numeric.cpp:48) and publication
+            if (fabs(ld_cg(rowg + static_cast<int64_t>(nl) * 32)) <= a.pivot_floor) atomicMin(a.failed + sc0 + lane, myrow);
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence();
+              st_relaxed_s32(a.flags + static_cast<int64_t>(myrow) * a.units + u, a.gen);
+            }
+          }
+        }
+        team_barrier(team);  // both members are done with the stage
+      }
+    }
+  }
+}
+
+}  // namespace b200lu

@@ -167,11 +167,25 @@ def test_batch_supernodal_form_is_bit_exact(rows, small, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("team", [0, 2, 4])
+def test_batch_row_block_kernels_agree(team, monkeypatch):
+    """B200LU_BATCH_TEAM: 0 = one warp per 2-row block (bfactor_block_kernel, the round-1 kernel), > 0 = one warp per row with
+    the pivot row staged once per block (bfactor_block_team_kernel, the default, here with other occupancy targets)."""
+    monkeypatch.setenv("B200LU_BATCH_TEAM", str(team))
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    _check_batch(kkt_fixture(700, 300, num_systems=4), 17, refine=False)
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+
+
+@needs_ref
 @pytest.mark.parametrize("contexts", [2, 4, 8])
 def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
     """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
     a context is left at the first pivot whose flag is not set instead of waited on). Off by default (slower)."""
     monkeypatch.setenv("B200LU_BATCH_MC", str(contexts))
+    monkeypatch.setenv("B200LU_BATCH_TEAM", "0")
     monkeypatch.setenv("B200LU_BATCH_TILES", "0")
     monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
     fx = kkt_fixture(700, 300, num_systems=4)
