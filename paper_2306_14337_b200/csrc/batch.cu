@@ -82,6 +82,7 @@ struct b200lu_batch {
   size_t block_smem = 0;
   void (*team_fn)(BBlockArgs) = nullptr;  // bfactor_block_team_kernel (blockteam.cuh): two warps per block
   int team_grid = 0;
+  size_t team_smem = 0;
   int mc_contexts = 0;  // > 0: bfactor_block_mc_kernel with that many block contexts per warp (blockmc.cuh)
   void (*mc_fn)(BBlockArgs, int) = nullptr;
   int mc_grid = 0;
@@ -431,7 +432,7 @@ b200lu_status launch_factor(H* h, int64_t* failed_rows) {
       bb.failed = h->d_failed;
       bb.ticket = h->d_tickets + 1;
       if (h->team_fn) {
-        h->team_fn<<<h->team_grid, kTeamWarps * 32, team_smem_bytes(), h->stream>>>(bb);
+        h->team_fn<<<h->team_grid, kTeamWarps * 32, h->team_smem, h->stream>>>(bb);
         ST_TRY(check_launch(h, "bfactor_block_team_kernel"));
       } else if (h->mc_contexts > 0) {
         h->mc_fn<<<h->mc_grid, 256, h->mc_smem, h->stream>>>(bb, h->mc_contexts);
@@ -1462,10 +1463,17 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
         using TFn = void (*)(BBlockArgs);
         TFn tfn = h->dest16 ? (minb >= 4 ? bfactor_block_team_kernel<uint16_t, 4> : minb == 3 ? bfactor_block_team_kernel<uint16_t, 3> : bfactor_block_team_kernel<uint16_t, 2>)
                             : bfactor_block_team_kernel<uint32_t, 2>;
+        h->team_smem = team_smem_bytes();
+        if (const char* e2 = std::getenv("B200LU_BATCH_TEAM_STAGES")) {  // 2: double-buffered stage (blockteam.cuh)
+          if (std::atoi(e2) == 2 && h->dest16) {
+            tfn = minb >= 3 ? bfactor_block_team2_kernel<uint16_t, 3> : bfactor_block_team2_kernel<uint16_t, 2>;
+            h->team_smem = team2_smem_bytes();
+          }
+        }
         h->team_fn = tfn;
-        CU_TRY(h, cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(team_smem_bytes())));
+        CU_TRY(h, cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h->team_smem)));
         int tocc = 0;
-        CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tfn, kTeamWarps * 32, team_smem_bytes()));
+        CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, tfn, kTeamWarps * 32, h->team_smem));
         h->team_grid = prop.multiProcessorCount * std::max(1, tocc);
       }
     }

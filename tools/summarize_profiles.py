@@ -89,7 +89,7 @@ def main():
     traffic = {}
     seen = set()
     for rep in reps:
-        for kr in ("factor_kernel", "factor_block_kernel", "factor_tile_kernel", "tri_kernel", "tail_kernel"):
+        for kr in ("factor_kernel", "factor_block_kernel", "factor_block_team_kernel", "factor_tile_kernel", "tri_kernel", "tail_kernel"):
             ms = raw_metrics(rep, kr)
             if not ms:
                 continue
@@ -99,7 +99,7 @@ def main():
                 for w in WANT:
                     if w in m:
                         md.append(f"  * {w} = {m[w][0]} {m[w][1]}")
-                if kr in ("factor_kernel", "factor_block_kernel", "factor_tile_kernel") and "dram__bytes_read.sum" in m and kr not in seen:
+                if kr in ("factor_kernel", "factor_block_kernel", "factor_block_team_kernel", "factor_tile_kernel") and "dram__bytes_read.sum" in m and kr not in seen:
                     # one refactorization = the head launch + the row-blocked trailing launch: their traffic adds up
                     seen.add(kr)
                     def mb(x):
