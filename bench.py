@@ -117,7 +117,7 @@ class ClockSampler:
         self.p = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "20", "-i", str(device_index)], stdout=self.f,
+                                       "-lms", os.environ.get("B200LU_BENCH_SMI_MS", "50"), "-i", str(device_index)], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
