@@ -651,7 +651,10 @@ struct BTriArgs {
 // (Tried in round 2: the row's column indices fetched 32 at a time by the lanes and broadcast with shuffles, to take the
 // dependent index load out of every gather — 2.5x SLOWER, L 5.3 ms and U 12.0 ms per step at C2 x 256 against 2.1 / 4.5:
 // the shuffles are convergence points inside the unrolled load batches and the loads no longer issue back to back.)
-constexpr int kTriChunk = 8;
+#ifndef B200LU_TRI_CHUNK
+#define B200LU_TRI_CHUNK 8
+#endif
+constexpr int kTriChunk = B200LU_TRI_CHUNK;  // entries whose loads are in flight together
 constexpr int kTriBufferedWide = 32, kTriBufferedChain = 96;
 constexpr size_t tri_upper_smem(int buffered, int warps = 8) { return static_cast<size_t>(warps) * buffered * 32 * sizeof(double); }
 
