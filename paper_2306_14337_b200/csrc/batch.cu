@@ -26,6 +26,7 @@
 #include "snode.cuh"
 #include "blockmc.cuh"
 #include "blockteam.cuh"
+#include "tristeam.cuh"
 
 using namespace b200lu;
 
@@ -151,6 +152,8 @@ struct b200lu_batch {
   int factor_grid = 0, tri_grid = 0, tri_grid_upper = 0, tri_grid_chain = 0;
   void (*chain_fn)(BTriArgs) = nullptr;  // U sweep, narrow leading levels
   int chain_warps = 8, chain_buf = kTriBufferedChain;
+  bool chain_team = false;  // the chain launch runs btri_upper_team_kernel (a team of warps per row)
+  int chain_team_size = 1;
   int32_t upper_chain_rows = 0;  // leading rows of the U level order handled by the chain launch
   size_t factor_smem = 0;
 
@@ -495,7 +498,7 @@ b200lu_status launch_upper(H* h, const double* y, double* x) {
   BTriArgs a = tri_args(h, h->d_upper_meta, y, x, 2);
   if (h->upper_chain_rows > 0) {  // the narrow leading levels: whole rows parked, one CTA per SM
     a.count = h->upper_chain_rows;
-    CU_TRY(h, launch_resident(h->chain_fn, h->tri_grid_chain, h->chain_warps * 32, tri_upper_smem(h->chain_buf, h->chain_warps), h->stream, a));
+    CU_TRY(h, launch_resident(h->chain_fn, h->tri_grid_chain, h->chain_warps * 32, tri_upper_smem(h->chain_buf, h->chain_team ? kTriTeams : h->chain_warps), h->stream, a));
     ST_TRY(check_launch(h, "btri_kernel<upper chain>"));
   }
   if (h->upper_chain_rows < h->n) {
@@ -1546,13 +1549,31 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
       h->chain_fn = h->chain_buf == 48 ? btri_kernel<true, 48> : h->chain_buf == 64 ? btri_kernel<true, 64>
                                                                                      : btri_kernel<true, kTriBufferedChain>;
     }
-    CU_TRY(h, cudaFuncSetAttribute(h->chain_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(tri_upper_smem(h->chain_buf, h->chain_warps))));
+    {
+      // two warps per row (tristeam.cuh) unless B200LU_BATCH_UTEAM=0; same buffer per row, 8 warps per CTA
+      const char* eu = std::getenv("B200LU_BATCH_UTEAM");
+      const int ts = eu ? std::atoi(eu) : 2;
+      if (ts == 2 || ts == 4) {
+        h->chain_warps = ts * kTriTeams;
+        const char* eb2 = std::getenv("B200LU_BATCH_UBUF");
+        // buffer per row: 64 entries (12 rows in flight per SM) for large batches, 96 (8 rows, but every row of the C-shaped
+        // patterns parked whole) for small ones, where the sweep is bound by the level-to-level latency. Measured per step
+        // (two sweeps, C2): 256 scenarios 3.6 ms with 64 / 4.2 with 96 / 5.6 with 48; 32 scenarios 2.40 / 2.03 / 4.83.
+        const int auto_buf = h->padded <= 64 ? 96 : 64;
+        h->chain_buf = eb2 && std::atoi(eb2) == 48 ? 48 : eb2 && std::atoi(eb2) == 96 ? 96 : eb2 && std::atoi(eb2) == 64 ? 64 : auto_buf;
+        h->chain_fn = ts == 4 ? btri_upper_team_kernel<64, 4>
+                    : h->chain_buf == 48 ? btri_upper_team_kernel<48, 2> : h->chain_buf == 96 ? btri_upper_team_kernel<96, 2> : btri_upper_team_kernel<64, 2>;
+        if (ts == 4) h->chain_buf = 64;
+        h->chain_team = true;
+        h->chain_team_size = ts;
+      }
+    }
+    const size_t chain_smem = tri_upper_smem(h->chain_buf, h->chain_team ? kTriTeams : h->chain_warps);
+    CU_TRY(h, cudaFuncSetAttribute(h->chain_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(chain_smem)));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, btri_kernel<false, kTriBufferedWide>, 256, 0));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, btri_kernel<true, kTriBufferedWide>, 256,
                                                             tri_upper_smem(kTriBufferedWide)));
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, h->chain_fn, h->chain_warps * 32,
-                                                            tri_upper_smem(h->chain_buf, h->chain_warps)));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, h->chain_fn, h->chain_warps * 32, chain_smem));
     h->tri_grid = prop.multiProcessorCount * std::max(1, o1);
     h->tri_grid_upper = prop.multiProcessorCount * std::max(1, o2);
     h->tri_grid_chain = prop.multiProcessorCount * std::max(1, o3);
