@@ -340,7 +340,9 @@ b200lu_status b200lu_batch_kkt_update(b200lu_batch* h, const double* d_y, int on
  * loop (src/cli.cpp:80-135): while batch k is factorized and solved, the inputs of batch k + 1 cross the bus
  * on a dedicated copy stream into the staging buffer that is not in use, and the solutions of batch k leave on
  * a third stream. Host buffers should be page-locked (cudaHostRegister / pinned allocation) for the copies
- * to overlap. Typical loop:
+ * to overlap; every buffer of these calls (values, right-hand sides, host_x_out) may also be memory of the handle's
+ * device, in which case the copies are device-to-device (a caller that keeps its systems in HBM gets the same
+ * submission without a host round trip between the steps). Typical loop:
  *     stage_inputs(v[0], b[0]);
  *     for k: if (k + 1 < K) stage_inputs(v[k+1], b[k+1]); refactorize_staged(); solve_refine_staged(.., x[k], ..);
  *     staged_wait();                  // x[k] may be read only after staged_wait (or after the next-but-one call)

@@ -320,7 +320,8 @@ class BatchedFactors:
 
     # -- staged (pipelined) submission ------------------------------------------
     def _host_ptr(self, a, width, what):
-        """Host buffer (numpy array or CPU torch tensor, ideally page-locked) -> (pointer, keepalive)."""
+        """Buffer of a staged call — numpy array or CPU torch tensor (ideally page-locked), or a CUDA tensor on the handle's
+        device — -> (pointer, keepalive)."""
         if a is None:
             return None, None
         if hasattr(a, "data_ptr") and not rlu._is_device_tensor(a):  # CPU torch tensor (pin_memory() keeps copies async)
@@ -328,8 +329,11 @@ class BatchedFactors:
             if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != self.batch * width:
                 raise rlu.DimensionError(f"{what}: expected a contiguous float64 [{self.batch}, {width}] tensor")
             return a.data_ptr(), a
-        if rlu._is_device_tensor(a):
-            raise rlu.Error(f"{what}: the staged calls take HOST buffers")
+        if rlu._is_device_tensor(a):  # memory of the handle's device: the staged copies are device-to-device then
+            import torch
+            if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != self.batch * width:
+                raise rlu.DimensionError(f"{what}: expected a contiguous float64 [{self.batch}, {width}] tensor")
+            return a.data_ptr(), a
         h = np.ascontiguousarray(a, dtype=np.float64)
         if h.size != self.batch * width:
             raise rlu.DimensionError(f"{what}: expected [{self.batch}, {width}] values, got {h.size}")

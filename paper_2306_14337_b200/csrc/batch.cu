@@ -1887,12 +1887,13 @@ b200lu_status b200lu_batch_stage_inputs(b200lu_batch* h, const double* host_valu
   CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_vals_used[buf], 0));
   CU_TRY(h, cudaStreamWaitEvent(h->copy_in, h->ev_rhs_used[buf], 0));
   if (host_values && h->nnz_source) {
+    // cudaMemcpyDefault: the buffer may be host memory (pinned for the copy to overlap) or memory of this device
     CU_TRY(h, cudaMemcpyAsync(h->d_stage_vals[buf], host_values, static_cast<size_t>(h->nnz_source) * h->batch * sizeof(double),
-                              cudaMemcpyHostToDevice, h->copy_in));
+                              cudaMemcpyDefault, h->copy_in));
   }
   if (host_rhs && h->n) {
     CU_TRY(h, cudaMemcpyAsync(h->d_stage_rhs[buf], host_rhs, static_cast<size_t>(h->n) * h->batch * sizeof(double),
-                              cudaMemcpyHostToDevice, h->copy_in));
+                              cudaMemcpyDefault, h->copy_in));
   }
   CU_TRY(h, cudaEventRecord(h->ev_in[buf], h->copy_in));
   if (host_values) h->vals_queue.push_back(buf);
@@ -1962,7 +1963,7 @@ b200lu_status b200lu_batch_solve_refine_staged(b200lu_batch* h, int refine, cons
   CU_TRY(h, cudaEventRecord(h->ev_x[buf], h->stream));
   CU_TRY(h, cudaStreamWaitEvent(h->copy_out, h->ev_x[buf], 0));
   CU_TRY(h, cudaMemcpyAsync(host_x_out, h->d_stage_x[buf], static_cast<size_t>(h->n) * h->batch * sizeof(double),
-                            cudaMemcpyDeviceToHost, h->copy_out));
+                            cudaMemcpyDefault, h->copy_out));  // host memory or memory of this device
   CU_TRY(h, cudaEventRecord(h->ev_x_out[buf], h->copy_out));
   return fail;
 }

@@ -421,6 +421,36 @@ def test_pattern_the_tiled_kernel_cannot_take_keeps_the_row_blocked_one(tiles_en
         f.close()
 
 
+def test_staged_pipeline_takes_device_buffers():
+    """The buffers of the staged calls may live on the handle's device (device-to-device copies on the copy streams):
+    same results as with host buffers and as the plain calls, bit for bit."""
+    import torch
+    fx = golden_fixture("kkt_small")
+    batch, steps = 7, 3
+    f = BatchedFactors(fx.sym, batch)
+    g = BatchedFactors(fx.sym, batch)
+    try:
+        seq = []
+        for k in range(steps):
+            vals, rhs = _scenarios(fx, batch)
+            seq.append((torch.from_numpy(vals * (1.0 + 0.0625 * k)).cuda(), torch.from_numpy(rhs * (1.0 + 0.5 * k)).cuda()))
+        outs = [torch.empty((batch, fx.n), dtype=torch.float64, device="cuda") for _ in range(steps)]
+        f.stage_inputs(seq[0][0], seq[0][1])
+        for k in range(steps):
+            if k + 1 < steps:
+                f.stage_inputs(seq[k + 1][0], seq[k + 1][1])
+            f.refactorize_staged()
+            f.solve_refine_staged(outs[k])
+        f.staged_wait()
+        for k in range(steps):
+            g.refactorize(seq[k][0])
+            xr, _ = g.fgmres_refine(seq[k][1], g.solve_system(seq[k][1]))
+            assert torch.equal(outs[k], xr), k
+    finally:
+        f.close()
+        g.close()
+
+
 def test_staged_pipeline_matches_the_plain_calls_bitwise():
     """The staged (pipelined) submission — inputs of batch k + 1 copied while batch k is processed, solutions
     leaving on their own stream — gives, for every batch of a sequence, exactly the results of the plain
