@@ -89,7 +89,7 @@ def main():
     traffic = {}
     seen = set()
     for rep in reps:
-        for kr in ("factor_kernel", "factor_block_kernel", "factor_block_team_kernel", "factor_tile_kernel", "tri_kernel", "tail_kernel"):
+        for kr in ("factor_kernel", "factor_block_kernel", "factor_block_team_kernel", "factor_tile_kernel", "tri_kernel", "tri_upper_team_kernel", "tail_kernel"):
             ms = raw_metrics(rep, kr)
             if not ms:
                 continue
