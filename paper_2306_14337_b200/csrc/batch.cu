@@ -1128,13 +1128,13 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
     //     paid per 8 scenarios, the row-blocked kernel's per 32).
     //   * bfactor_block_kernel (batch.cuh): 2-row blocks x 32 scenarios, updates as L2 reductions: the faster
     //     one once the batch is THROUGHPUT-bound.
-    // B200LU_BATCH_TILES = 1 / 0 forces one of them; default: tiles up to 96 scenarios per handle (an 8-GPU
-    // shard of the 256-scenario batch is 32), provided two tile CTAs fit on an SM (setup_tiles). A pattern / batch the tiled kernel cannot take (a row larger than
+    // B200LU_BATCH_TILES = 1 / 0 forces one of them; default: tiles up to 32 scenarios per handle (an 8-GPU
+    // shard of the 256-scenario batch; up to 96 while the row-blocked kernel ran one warp per block), provided two tile CTAs fit on an SM (setup_tiles). A pattern / batch the tiled kernel cannot take (a row larger than
     // a tile, a pivot row longer than a staging copy, more than 2^31 entries per tensor-map dimension) keeps
     // the row-blocked kernel.
     e = std::getenv("B200LU_BATCH_TILES");
     const bool forced = e != nullptr;
-    const bool want_tiles = forced ? std::atoi(e) != 0 : h->padded <= 96;
+    const bool want_tiles = forced ? std::atoi(e) != 0 : h->padded <= 32;  // against the one-warp-per-row kernel (factor phase, C2): 32 scenarios 4.85 / 5.82 ms, 64: 7.95 / 7.67, 96: 11.0 / 9.8, 128: 14.8 / 12.5
     h->tile_auto = !forced;
     // (Running both side by side — the tiled kernel on some of the scenarios, the row-blocked one on the rest, one
     // CTA of each per SM on two streams — was measured at C2 x 256: 35-46 ms against 24.4 ms for the row-blocked
