@@ -80,7 +80,8 @@ bfactor_block_team_kernel(const BBlockArgs a) {
         const int32_t ns = min(m + 1, kBlockStage);  // staged entries of the pivot row (diagonal included)
         // member 0 awaits the pivot row's flag and stages it for the team; each member stages its own destination slice
         if (me == 0) {
-          if (!__shfl_sync(full, my_ready, q)) {
+          // (a pivot that is a row of this block — bit 16 — is member 0's own row, published earlier in program order)
+          if (!__shfl_sync(full, my_ready, q) && !(bits & 0x10000u)) {
             const int32_t d = __shfl_sync(full, my_d, q);
             wait_flag(a.flags + static_cast<int64_t>(d) * a.units + u, a.gen);
           }
