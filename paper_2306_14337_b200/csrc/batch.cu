@@ -1575,6 +1575,9 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
                                                             tri_upper_smem(kTriBufferedWide)));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, h->chain_fn, h->chain_warps * 32, chain_smem));
     h->tri_grid = prop.multiProcessorCount * std::max(1, o1);
+    if (const char* eg = std::getenv("B200LU_BATCH_LGRID")) {  // experiment: fewer resident CTAs in the L sweep
+      if (std::atoi(eg) > 0) h->tri_grid = std::min(h->tri_grid, std::atoi(eg));
+    }
     h->tri_grid_upper = prop.multiProcessorCount * std::max(1, o2);
     h->tri_grid_chain = prop.multiProcessorCount * std::max(1, o3);
     // experiment: fewer resident CTAs in the U sweep. Measured at C2 x 256 (two sweeps per step): 444 CTAs 4.53 ms, 296: 5.76,
