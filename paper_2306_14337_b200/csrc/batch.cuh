@@ -660,11 +660,8 @@ constexpr size_t tri_upper_smem(int buffered, int warps = 8) { return static_cas
 
 // (The L sweep is residency-sensitive — 2.10 / 2.57 / 4.29 ms per step with 444 / 296 / 148 CTAs at C2 x 256 — but forcing four or
 // five CTAs per SM costs spills: 2.44 / 2.40 ms, and 1.48 / 1.24 ms against 1.09 at 32 scenarios. Three CTAs, 70 registers.)
-#ifndef B200LU_TRI_LOWER_MINB
-#define B200LU_TRI_LOWER_MINB 1
-#endif
 template <bool kUpper, int kTriBuffered>
-__global__ void __launch_bounds__(256, kUpper ? 1 : B200LU_TRI_LOWER_MINB)
+__global__ void __launch_bounds__(256)
 btri_kernel(const BTriArgs a) {
   extern __shared__ __align__(16) double tri_smem[];
   const int lane = threadIdx.x & 31;
