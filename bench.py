@@ -39,6 +39,7 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 import numpy as np
@@ -106,25 +107,76 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region: NVML read from a thread of this process every
+    5 ms (the counters `nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.*` prints — a separate
+    nvidia-smi process needs ~0.5 s before its first sample, longer than a default timed region), nvidia-smi -lms as
+    the fallback when NVML cannot be loaded. `window()` brackets the timed steps: only samples taken inside it count."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+            0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device_index):
+        self.samples, self.t0, self.t1 = [], None, None   # (time, sm MHz, max sm MHz, reason bits)
+        self.p = self.f = self.thread = None
+        self.stop_flag = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[device_index]) if vis and vis.split(",")[device_index].isdigit() else device_index
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            period = float(os.environ.get("B200LU_BENCH_SMI_MS", "5")) / 1e3
+
+            def run():
+                while not self.stop_flag.is_set():
+                    try:
+                        self.samples.append((time.perf_counter(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                             smax, int(reasons_fn(h))))
+                    except Exception:
+                        pass
+                    self.stop_flag.wait(period)
+            self.source = "nvml"
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
+        self.source = "nvidia-smi"
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", os.environ.get("B200LU_BENCH_SMI_MS", "50"), "-i", str(device_index)], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
+                                       "-lms", "20", "-i", str(device_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.6)   # its first sample takes that long
         except Exception:
             self.p = None
 
+    def window_start(self):
+        self.t0 = time.perf_counter()
+
+    def window_stop(self):
+        self.t1 = time.perf_counter()
+
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            inside = [s for s in self.samples if self.t0 is not None and self.t0 <= s[0] <= (self.t1 or 1e300)]
+            use = inside or self.samples
+            bits = 0
+            for s in use:
+                bits |= s[3]
+            return {"sm_mhz": statistics.median([s[1] for s in use]) if use else None,
+                    "sm_max_mhz": max(s[2] for s in use) if use else None, "samples": len(use),
+                    "samples_inside_timed_region": len(inside), "source": "nvml, 5 ms period, thread of the bench process",
+                    "reasons": sorted(nm for b, nm in self.BITS.items() if bits & b)}
         if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml and nvidia-smi unavailable"]}
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
@@ -145,7 +197,7 @@ class ClockSampler:
             except Exception:
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "source": "nvidia-smi -lms 20", "reasons": sorted(reasons)}
 
 
 def nccl_init_lines():
@@ -320,6 +372,8 @@ def measure_single(args, workload, steps, with_cpu_baseline):
             dist.barrier()
         torch.cuda.synchronize()
         sampler = ClockSampler(local_rank) if sample_clocks else None
+        if sampler:
+            sampler.window_start()
         f.set_timing(True)
         launches0 = f.launch_count
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -334,6 +388,8 @@ def measure_single(args, workload, steps, with_cpu_baseline):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        if sampler:
+            sampler.window_stop()
         clocks = sampler.stop() if sampler else None
         per_step = [a.elapsed_time(b) for a, b in ev]
         phases = f.phase_times()
@@ -453,6 +509,77 @@ def measure_single(args, workload, steps, with_cpu_baseline):
     return line
 
 
+def measure_c3_batch(args, scenarios=64, steps=5, warmup=3):
+    """The bandwidth-bound C3 figure: `scenarios` C3-shaped scenario systems (one pattern, y_seed = 2 + scenario) per
+    step through the scenario-batch kernels, buffers resident in HBM, K steps through the staged submission calls under
+    one event pair — the C3 counterpart of the headline, next to `single_system` (one C3 system alone, latency-bound)."""
+    import torch
+
+    import paper_2306_14337_b200 as rlu
+    from paper_2306_14337_b200.batch import BatchedFactors
+    from oracle import refbridge as rb  # input fixtures only
+
+    _, local_rank, _ = dist_env()
+    n, m, desc = WORKLOADS["C3"]
+    seqs = [rb.RefSequence(n, m, y_seed=2 + sc, num_systems=1) for sc in range(scenarios)]
+    sym, ref_sym, _ = analyze_for_bench(rlu, rb, seqs[0].matrix(0), np)
+    N, nnz_a, nnz_f = seqs[0].n, seqs[0].nnz, ref_sym.nnz_factors
+    stream = torch.cuda.current_stream()
+    f = BatchedFactors(sym, scenarios, rlu.FactorOptions(device=local_rank, stream=stream.cuda_stream,
+                                                         refine_capacity=args.refine_maxit))
+    cfg = rlu.RefineConfig(args.refine_maxit, args.refine_tol)
+    dev_vals = torch.from_numpy(np.stack([q.values(0) for q in seqs])).cuda()
+    dev_rhs = torch.from_numpy(np.stack([q.rhs(0) for q in seqs])).cuda()
+    outs = [torch.empty((scenarios, N), dtype=torch.float64, device="cuda") for _ in range(2)]
+
+    def loop(K):
+        f.stage_inputs(dev_vals, dev_rhs)
+        for k in range(K):
+            if k + 1 < K:
+                f.stage_inputs(dev_vals, dev_rhs)
+            f.refactorize_staged()
+            f.solve_refine_staged(outs[k % 2], cfg, refine=not args.no_refine)
+        f.staged_wait()
+    loop(max(2, warmup))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    loop(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    # per-phase times and the residuals through the synchronous calls
+    f.set_timing(True)
+    f.refactorize(dev_vals)
+    x = f.solve_system(dev_rhs)
+    its = [0] * scenarios
+    if not args.no_refine:
+        x, ro = f.fgmres_refine(dev_rhs, x, cfg)
+        its = [o.iterations for o in ro]
+    torch.cuda.synchronize()
+    phases = f.phase_times()
+    f.set_timing(False)
+    worst = float(f.relative_residual(x, dev_rhs).max())
+    ab = batch_algorithmic_bytes(scenarios, N, nnz_a, nnz_f, int(statistics.median(its)))
+    peak, peak_src = measured_peak()
+    fac_ms = phases["factor"][0] / max(phases["factor"][1], 1)
+    info = f.info
+    f.close()
+    return {"value": scenarios / (ms / 1000.0), "unit": UNIT, "ms_per_step": ms, "ms_per_system": ms / scenarios,
+            "steps": steps, "warmup": warmup,
+            "config": {"workload": f"C3 x {scenarios}: {scenarios} independent {desc} scenario systems in one batch on one GPU, "
+                                   "same step as the headline (scatter + refactorize + solve_system + fgmres_refine) through "
+                                   "the staged submission calls, buffers resident in HBM",
+                       "n": N, "nnz": nnz_a, "nnz_factors": nnz_f, "device_gb": round(info["device_bytes"] / 1e9, 2)},
+            "phases_ms": {p: v[0] for p, v in phases.items()}, "refine_iters_median": int(statistics.median(its)),
+            "relres_final_max": worst,
+            "roofline": {"kernel": "batched K2 refactorization (head + trailing launch)", "bound": "hbm",
+                         "achieved": ab["eliminate"] / (fac_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": ab["eliminate"] / (fac_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_ms,
+                         "whole_step_frac": ab["total"] / (ms * 1e-3) / 1e9 / peak}}
+
+
 def reference_batch_sample(rb, ref_sym, seqs, threads, refine=True, max_iterations=20, tolerance=1e-14):
     """The reference on a block of independent scenarios: one scenario per host thread, each through
     reset_values + factorize_scattered + solve_system + fgmres_refine in ExecMode::sequential (the
@@ -565,7 +692,7 @@ def run_batch(args):
 
     dev_xs = [torch.empty((S, N), dtype=torch.float64, device="cuda") for _ in range(2)]
 
-    def timed_pipelined(steps, warmup, resident=False):
+    def timed_pipelined(steps, warmup, resident=False, sampler=None):
         """K batches through the staged submission calls (b200lu_batch_stage_inputs / refactorize_staged /
         solve_refine_staged) under ONE event pair. resident=False is the e2e number: HOST buffers, every step's values
         and right-hand sides copied H2D from pinned memory and its solutions D2H, all inside the timed region; the
@@ -587,10 +714,14 @@ def run_batch(args):
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if sampler:
+            sampler.window_start()
         e0.record()
         loop(steps)
         e1.record()
         torch.cuda.synchronize()
+        if sampler:
+            sampler.window_stop()
         if world > 1:
             dist.barrier()
         return e0.elapsed_time(e1)
@@ -618,6 +749,8 @@ def run_batch(args):
             dist.barrier()
         torch.cuda.synchronize()
         sampler = ClockSampler(local_rank) if sample_clocks else None
+        if sampler:
+            sampler.window_start()
         f.set_timing(True)
         launches0 = f.info["launches"]
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -631,6 +764,8 @@ def run_batch(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        if sampler:
+            sampler.window_stop()
         clocks = sampler.stop() if sampler else None
         phases = f.phase_times()
         f.set_timing(False)
@@ -642,7 +777,7 @@ def run_batch(args):
     pipelined_same = bool(torch.equal(host_xs[(args.steps - 1) % 2], step_e2e()[0]))  # same bits as the plain calls
     # `value`: the same K steps with every buffer resident in HBM, through the same staged calls (clocks sampled here too)
     sampler_res = ClockSampler(local_rank)
-    res_total_ms = timed_pipelined(args.steps, args.warmup, resident=True)
+    res_total_ms = timed_pipelined(args.steps, args.warmup, resident=True, sampler=sampler_res)
     clocks_res = sampler_res.stop()
     resident_same = bool(torch.equal(dev_xs[(args.steps - 1) % 2], step_resident()[0]))
     kkt_total_ms, _, _, _, _ = timed(step_e2e_kkt, args.steps, max(1, args.warmup // 2), False)
@@ -668,8 +803,10 @@ def run_batch(args):
     total_ms_max, e2e_ms_max, relres_max, kkt_ms_max, e2e_serial_max, res_ms_max = (float(v) for v in t.cpu())
 
     # the single-system measurements ride on the N = 1 line only (they do not shard)
-    single = c4 = None
+    single = c4 = c3b = None
     if not args.no_single and world == 1:
+        if not args.no_c3_batch:
+            c3b = measure_c3_batch(args)
         single = measure_single(args, args.single_workload, min(args.steps * 2, 20), False)
         if not args.no_c4:
             c4 = measure_single(args, "C4", min(args.steps, 10), False)
@@ -771,6 +908,8 @@ def run_batch(args):
         if c4 is not None:
             line["c4"] = {k: c4[k] for k in keys}
             line["c4"]["analysis"] = c4.get("analysis")
+        if c3b is not None:
+            line["c3_batch"] = c3b
         if nccl_lines is not None:
             line["nccl"] = nccl_lines
         if not args.no_cpu_baseline:  # rank 0, at every N: the reference on this box's host cores
@@ -887,6 +1026,7 @@ def main():
     ap.add_argument("--scenarios", type=int, default=256, help="C5: scenarios of the batch in TOTAL, sharded over the GPUs")
     ap.add_argument("--scenarios-per-gpu", type=int, default=0, help="C5: fix the per-GPU batch instead (weak scaling)")
     ap.add_argument("--no-c4", action="store_true", help="C5: skip the C4 (n = 1.6 M) single-system block")
+    ap.add_argument("--no-c3-batch", action="store_true", help="C5: skip the C3 x 64 scenario-batch block")
     ap.add_argument("--single-workload", default="C3", choices=sorted(WORKLOADS),
                     help="C5: the single-system measurement reported next to the batch")
     ap.add_argument("--no-single", action="store_true", help="C5: skip the single-system measurement")
