@@ -113,19 +113,38 @@ __global__ void __launch_bounds__(256)
 bscatter_kernel(int64_t nnz_factors, int64_t nnz_source, int32_t groups,
                 const int32_t* __restrict__ src_of_slot, const double* __restrict__ a_int,
                 const double* __restrict__ scatter_scale, double* __restrict__ values) {
+  // a warp takes FOUR consecutive slots per step: one 16-byte load of their source indices, the (few) source values
+  // requested together, four 256-byte stores — a quarter of the dependent index -> value -> store round trips of the
+  // slot-per-step form (scatter phase at C2 x 256 incl. the layout change: 1.63 -> 1.13 ms)
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t total = nnz_factors * groups;
+  const int64_t quads = (nnz_factors + 3) >> 2;
+  const int64_t total = quads * groups;
   for (int64_t t = warp; t < total; t += nwarps) {
-    const int64_t g = t / nnz_factors, s = t - g * nnz_factors;
-    const int32_t k = __ldg(src_of_slot + s);
-    double v = 0.0;
-    if (k >= 0) {
-      v = a_int[(g * nnz_source + k) * 32 + lane];
-      if (scatter_scale != nullptr) v = __dmul_rn(v, __ldg(scatter_scale + k));
+    const int64_t g = t / quads, s0 = (t - g * quads) << 2;
+    int32_t k[4];
+    if (s0 + 3 < nnz_factors) {
+      const int4 k4 = __ldg(reinterpret_cast<const int4*>(src_of_slot + s0));
+      k[0] = k4.x, k[1] = k4.y, k[2] = k4.z, k[3] = k4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k[j] = s0 + j < nnz_factors ? __ldg(src_of_slot + s0 + j) : -2;
     }
-    values[t * 32 + lane] = v;
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = k[j] >= 0 ? a_int[(g * nnz_source + k[j]) * 32 + lane] : 0.0;
+    if (scatter_scale != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (k[j] >= 0) v[j] = __dmul_rn(v[j], __ldg(scatter_scale + k[j]));
+      }
+    }
+    double* out = values + (g * nnz_factors + s0) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (k[j] != -2) out[j * 32] = v[j];
+    }
   }
 }
 
