@@ -322,7 +322,7 @@ const double* hscal(const H* h, int slot) { return h->h_scal + static_cast<size_
 b200lu_status launch_scatter(H* h) {
   if (h->nnz_factors == 0) return B200LU_OK;
   PhaseScope ps(h, B200LU_PHASE_SCATTER);
-  const int blocks = std::min<int64_t>(blocks_for(((h->nnz_factors + 3) / 4) * h->groups * 32, 256), 148 * 16);
+  const int blocks = std::min<int64_t>(blocks_for(((h->nnz_factors + kScatterSlots - 1) / kScatterSlots) * h->groups * 32, 256), 148 * 16);
   bscatter_kernel<<<blocks, 256, 0, h->stream>>>(h->nnz_factors, h->nnz_source, h->groups, h->d_src_of_slot, h->d_a_int,
                                                  h->d_scatter_scale, h->d_values);
   return check_launch(h, "bscatter_kernel");

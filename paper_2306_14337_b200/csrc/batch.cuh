@@ -109,40 +109,51 @@ deinterleave_kernel(int64_t len, int32_t batch, const double* __restrict__ src, 
 //
 // scatter_values (src/numeric.cpp:19-22) for every scenario: gather form through the inverse
 // map, fill slots exactly 0, one coalesced 256-byte store per (slot, group).
+#ifndef B200LU_SCATTER_SLOTS
+#define B200LU_SCATTER_SLOTS 4
+#endif
+constexpr int kScatterSlots = B200LU_SCATTER_SLOTS;  // consecutive slots a warp takes per step (a multiple of 4)
+static_assert(kScatterSlots % 4 == 0 && kScatterSlots >= 4, "index loads are 16 bytes");
+
 __global__ void __launch_bounds__(256)
 bscatter_kernel(int64_t nnz_factors, int64_t nnz_source, int32_t groups,
                 const int32_t* __restrict__ src_of_slot, const double* __restrict__ a_int,
                 const double* __restrict__ scatter_scale, double* __restrict__ values) {
-  // a warp takes FOUR consecutive slots per step: one 16-byte load of their source indices, the (few) source values
-  // requested together, four 256-byte stores — a quarter of the dependent index -> value -> store round trips of the
-  // slot-per-step form (scatter phase at C2 x 256 incl. the layout change: 1.63 -> 1.13 ms)
+  // a warp takes kScatterSlots consecutive slots per step: 16-byte loads of their source indices, the (few) source
+  // values requested together, 256-byte stores — a quarter of the dependent index -> value -> store round trips of the
+  // slot-per-step form (scatter phase at C2 x 256 incl. the layout change: 1.63 -> 1.10 ms; 8 slots 1.08, 16 slots 1.05:
+  // the 4.5 GB of stores are what is left)
+  constexpr int S = kScatterSlots;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t quads = (nnz_factors + 3) >> 2;
-  const int64_t total = quads * groups;
+  const int64_t chunks = (nnz_factors + S - 1) / S;
+  const int64_t total = chunks * groups;
   for (int64_t t = warp; t < total; t += nwarps) {
-    const int64_t g = t / quads, s0 = (t - g * quads) << 2;
-    int32_t k[4];
-    if (s0 + 3 < nnz_factors) {
-      const int4 k4 = __ldg(reinterpret_cast<const int4*>(src_of_slot + s0));
-      k[0] = k4.x, k[1] = k4.y, k[2] = k4.z, k[3] = k4.w;
+    const int64_t g = t / chunks, s0 = (t - g * chunks) * S;
+    int32_t k[S];
+    if (s0 + S <= nnz_factors) {
+#pragma unroll
+      for (int q = 0; q < S / 4; ++q) {
+        const int4 k4 = __ldg(reinterpret_cast<const int4*>(src_of_slot + s0) + q);
+        k[4 * q] = k4.x, k[4 * q + 1] = k4.y, k[4 * q + 2] = k4.z, k[4 * q + 3] = k4.w;
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) k[j] = s0 + j < nnz_factors ? __ldg(src_of_slot + s0 + j) : -2;
+      for (int j = 0; j < S; ++j) k[j] = s0 + j < nnz_factors ? __ldg(src_of_slot + s0 + j) : -2;  // -2: no such slot
     }
-    double v[4];
+    double v[S];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = k[j] >= 0 ? a_int[(g * nnz_source + k[j]) * 32 + lane] : 0.0;
+    for (int j = 0; j < S; ++j) v[j] = k[j] >= 0 ? a_int[(g * nnz_source + k[j]) * 32 + lane] : 0.0;
     if (scatter_scale != nullptr) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < S; ++j) {
         if (k[j] >= 0) v[j] = __dmul_rn(v[j], __ldg(scatter_scale + k[j]));
       }
     }
     double* out = values + (g * nnz_factors + s0) * 32 + lane;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < S; ++j) {
       if (k[j] != -2) out[j * 32] = v[j];
     }
   }
