@@ -1467,6 +1467,13 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
         TFn tfn = h->dest16 ? (minb >= 4 ? bfactor_block_team_kernel<uint16_t, 4> : minb == 3 ? bfactor_block_team_kernel<uint16_t, 3> : bfactor_block_team_kernel<uint16_t, 2>)
                             : bfactor_block_team_kernel<uint32_t, 2>;
         h->team_smem = team_smem_bytes();
+        // pivot rows staged by ONE bulk asynchronous copy per pivot (cp.async.bulk + mbarrier, blockteam.cuh) — the default;
+        // B200LU_BATCH_TEAM_BULK=0 restores the per-lane 16-byte cp.async (22.0 against 22.3 ms at C2 x 256, equal at 32)
+        const char* eb = std::getenv("B200LU_BATCH_TEAM_BULK");
+        if (!eb || std::atoi(eb) != 0) {
+          tfn = h->dest16 ? (minb >= 4 ? bfactor_block_team_kernel<uint16_t, 4, true> : minb == 3 ? bfactor_block_team_kernel<uint16_t, 3, true> : bfactor_block_team_kernel<uint16_t, 2, true>)
+                          : bfactor_block_team_kernel<uint32_t, 2, true>;
+        }
         if (const char* e2 = std::getenv("B200LU_BATCH_TEAM_STAGES")) {  // 2: double-buffered stage (blockteam.cuh)
           if (std::atoi(e2) == 2 && h->dest16) {
             tfn = minb >= 3 ? bfactor_block_team2_kernel<uint16_t, 3> : bfactor_block_team2_kernel<uint16_t, 2>;

@@ -23,7 +23,30 @@ __device__ __forceinline__ void team_barrier(int team) {
   asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(32 * kTeamSize) : "memory");
 }
 
-template <typename DestT, int MINB>
+// BULK = true: the pivot row — one contiguous block of (m + 1) x 256 bytes — is staged by ONE bulk asynchronous copy
+// (cp.async.bulk, the 1-D form of TMA: SASS UBLKCP) issued by lane 0 of member 0 and awaited on an mbarrier, instead of
+// ns / 2 16-byte cp.async per lane. The row was written by other SMs through the generic proxy (reductions, st.cg) and is
+// read here by the async proxy: fence.proxy.async.global between the acquired flag and the copy.
+__device__ __forceinline__ uint32_t team_smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void team_mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t addr = team_smem_u32(bar);
+  while (!ok) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(addr), "r"(parity)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void team_bulk_copy(double* stage, const double* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(team_smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(team_smem_u32(stage)), "l"(src), "r"(bytes), "r"(team_smem_u32(bar))
+               : "memory");
+}
+
+template <typename DestT, int MINB, bool BULK = false>
 __global__ void __launch_bounds__(kTeamWarps * 32, MINB)
 bfactor_block_team_kernel(const BBlockArgs a) {
   static_assert(kBlockStage > 0, "the team variant stages the pivot rows");
@@ -35,6 +58,15 @@ bfactor_block_team_kernel(const BBlockArgs a) {
   double* stage = team_smem + static_cast<size_t>(team) * team_stage_doubles();
   unsigned long long* tslot = reinterpret_cast<unsigned long long*>(team_smem + kTeams * team_stage_doubles()) + team * 2;
   const unsigned long long total = static_cast<unsigned long long>(a.n_blocks) * a.units_here;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tslot + 1);  // BULK: arrival of the staged pivot row
+  uint32_t ph = 0;                                         // its phase parity: one completion per staged pivot
+  if constexpr (BULK) {
+    if (me == 0 && lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(team_smem_u32(bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    team_barrier(team);
+  }
   while (true) {
     if (me == 0 && lane == 0) *tslot = atomicAdd(a.ticket, 1ull);
     team_barrier(team);
@@ -87,7 +119,11 @@ bfactor_block_team_kernel(const BBlockArgs a) {
           }
           __syncwarp();
           const double* src = ug - lane;
-          for (int32_t t16 = lane; t16 < ns * 16; t16 += 32) cp_async_16(stage + t16 * 2, src + t16 * 2);
+          if constexpr (BULK) {
+            if (lane == 0) team_bulk_copy(stage, src, static_cast<uint32_t>(ns) * 256u, bar);
+          } else {
+            for (int32_t t16 = lane; t16 < ns * 16; t16 += 32) cp_async_16(stage + t16 * 2, src + t16 * 2);
+          }
         }
         if (mine) {
           const char* dsrc = reinterpret_cast<const char*>(dest + p);
@@ -101,6 +137,10 @@ bfactor_block_team_kernel(const BBlockArgs a) {
         if (mine) nalpha = ld_cg(rowg + static_cast<int64_t>(k) * 32);
         cp_async_commit_wait_all();
         team_barrier(team);  // the stage is filled (and member 0 has acquired the pivot row's flag for both)
+        if constexpr (BULK) {  // ... or, with the bulk copy, issued: every thread awaits its arrival
+          team_mbar_wait(bar, ph);
+          ph ^= 1u;
+        }
         if (mine) {
           const double udd = stage[lane];
           nalpha = -(nalpha / udd);  // src/numeric.cpp:40; the sign is exact

@@ -180,6 +180,27 @@ def test_batch_row_block_kernels_agree(team, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("bulk", [0, 1])
+def test_batch_team_kernel_staging_modes_agree(bulk, monkeypatch):
+    """B200LU_BATCH_TEAM_BULK: 1 (default) = the pivot row staged by one cp.async.bulk per pivot, awaited on an mbarrier;
+    0 = per-lane 16-byte cp.async. Same values bit for bit, incl. pivot rows longer than the stage and partial groups."""
+    monkeypatch.setenv("B200LU_BATCH_TEAM_BULK", str(bulk))
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    _check_batch(kkt_fixture(700, 300, num_systems=4), 33, refine=False)
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+    n, band = 150, 70  # pivot rows of up to 70 upper entries: the part beyond the 48-entry stage goes through registers
+    M = np.zeros((n, n))
+    rng = np.random.default_rng(5)
+    for i in range(n):
+        lo, hi = max(0, i - band), min(n, i + band + 1)
+        M[i, lo:hi] = rng.uniform(-1.0, 1.0, hi - lo)
+        M[i, i] = 2.0 * band + 1.0
+    _check_batch(dense_fixture(M), 9, refine=False)
+
+
+@needs_ref
 @pytest.mark.parametrize("contexts", [2, 4, 8])
 def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
     """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
