@@ -33,7 +33,8 @@ __device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
 }
 // Spins until the (row, unit) flag reaches `gen`. The poll is paced (sleep doubling from 32 ns to
 // 256 ns): a stalled dependency chain leaves most resident warps waiting, and unpaced polls — tens
-// per microsecond and warp — compete with the working warps for the load/store path.
+// per microsecond and warp — compete with the working warps for the load/store path. (Relaxed polls followed by ONE acquire
+// load once the flag is seen set — no L1 invalidation per poll — measured the same: 22.2 / 5.70 ms at 256 / 32 scenarios.)
 __device__ __forceinline__ int32_t ld_flag_poll(const int32_t* p) {
 #ifdef B200LU_POLL_ATOMIC
   return atomicOr(const_cast<int32_t*>(p), 0);
