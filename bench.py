@@ -1037,6 +1037,12 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    # torchrun exports OMP_NUM_THREADS=1 to every rank unless the caller set it; the CPU arm (rank 0 alone: `--impl
+    # reference`, and `cpu_baseline`) is to run on all the host threads it can use, so that default is undone before
+    # libgomp is loaded (B200LU_BENCH_THREADS overrides the count)
+    want = os.environ.get("B200LU_BENCH_THREADS")
+    if want or ("TORCHELASTIC_RUN_ID" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1"):
+        os.environ["OMP_NUM_THREADS"] = want or str(len(os.sched_getaffinity(0)))
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
         # self-launch: one rank per GPU on this node (rendezvous on 127.0.0.1: the hostname may not resolve)
         import socket
