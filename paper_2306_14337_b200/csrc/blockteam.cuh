@@ -11,6 +11,10 @@
 
 #include "batch.cuh"
 
+#ifndef B200LU_TEAM_RMW
+#define B200LU_TEAM_RMW 0
+#endif
+
 namespace b200lu {
 
 constexpr int kTeamWarps = 8;                        // warps per CTA
@@ -146,6 +150,28 @@ bfactor_block_team_kernel(const BBlockArgs a) {
           nalpha = -(nalpha / udd);  // src/numeric.cpp:40; the sign is exact
           const char* dbytes = reinterpret_cast<const char*>(stage + kBlockStage * 32 + me * kBlockStageDest);
           const DestT* dl = reinterpret_cast<const DestT*>(dbytes + (reinterpret_cast<uintptr_t>(dest + p) & 3));
+#if B200LU_TEAM_RMW > 0
+          // experiment (off): every B200LU_TEAM_RMW-th pivot of a row updates through L2 loads and stores instead of L2
+          // reductions (same two roundings; same thread per address, program order) to move work off the L2 atomic unit.
+          // Bit-exact, and slower the more pivots take this path — C2 x 256, factor phase: every 2nd pivot 26.5 ms, 3rd 24.5,
+          // 4th 23.4, 6th 22.6, none 22.2 (32 scenarios: 6.6 against 5.75): the round trip per load batch costs more than
+          // the atomic unit gains
+          if (k % B200LU_TEAM_RMW == B200LU_TEAM_RMW - 1) {
+            for (int32_t cs = 0; cs < ns - 1; cs += 8) {
+              double v[8];
+              double* ap[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                ap[j] = rowg + static_cast<int64_t>(dl[min(cs + j, ns - 2)]) * 32;
+                v[j] = ld_cg(ap[j]);
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (cs + j < ns - 1) st_cg(ap[j], __dadd_rn(v[j], __dmul_rn(nalpha, stage[(1 + cs + j) * 32 + lane])));
+              }
+            }
+          } else
+#endif
 #pragma unroll 4
           for (int32_t cs = 0; cs < ns - 1; ++cs) {
             red_add_f64(rowg + static_cast<int64_t>(dl[cs]) * 32, __dmul_rn(nalpha, stage[(1 + cs) * 32 + lane]));  // src/numeric.cpp:44
