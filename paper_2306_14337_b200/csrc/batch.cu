@@ -1396,7 +1396,9 @@ b200lu_status b200lu_batch_create(const b200lu_symbolic_view* sym, const b200lu_
   CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_up), static_cast<size_t>(kUpSlots) * P * sizeof(double)));
   CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_failed), 2 * P * sizeof(int32_t)));
 
-  h->dest16 = S.max_row_len <= 65535;
+  // destinations are 16-bit offsets into the row unless a row has more than 65 535 entries; B200LU_BATCH_DEST32=1 forces
+  // the 32-bit instantiations (test knob: no pattern of the configs comes near that row length)
+  h->dest16 = S.max_row_len <= 65535 && !(std::getenv("B200LU_BATCH_DEST32") && std::atoi(std::getenv("B200LU_BATCH_DEST32")) == 1);
   ST_TRY(dev_alloc(h, reinterpret_cast<char**>(&h->d_dest), static_cast<size_t>(S.update_pairs) * (h->dest16 ? 2 : 4) + 256));  // slack: chunk copies read whole words
   if (n > 0 && S.update_pairs > 0) {
     const int blocks = std::min<int64_t>(blocks_for(n * 32, 256), 148 * 32);

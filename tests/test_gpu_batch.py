@@ -201,6 +201,21 @@ def test_batch_team_kernel_staging_modes_agree(bulk, monkeypatch):
 
 
 @needs_ref
+@pytest.mark.parametrize("team", [0, 3])
+def test_batch_32_bit_destination_tables(team, monkeypatch):
+    """Rows of more than 65 535 entries need 32-bit destination offsets; no config has such a row, so the uint32_t
+    instantiations of the refactorization kernels are forced here (B200LU_BATCH_DEST32=1) and checked bit for bit."""
+    monkeypatch.setenv("B200LU_BATCH_DEST32", "1")
+    monkeypatch.setenv("B200LU_BATCH_TILES", "0")  # the tiled kernel has its own destination table
+    monkeypatch.setenv("B200LU_BATCH_TEAM", str(team))
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "100000")
+    _check_batch(kkt_fixture(700, 300, num_systems=4), 33, refine=False)
+    _check_batch(golden_fixture("random_sparse_120_plain"), 5, refine=False)
+    monkeypatch.setenv("B200LU_BATCH_TAIL_WIDTH", "0")  # everything through the row-per-warp head kernel
+    _check_batch(kkt_fixture(700, 300, num_systems=3, use_scaling=True), 7, refine=False)
+
+
+@needs_ref
 @pytest.mark.parametrize("contexts", [2, 4, 8])
 def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
     """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
