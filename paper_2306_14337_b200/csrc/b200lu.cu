@@ -917,7 +917,8 @@ b200lu_status b200lu_create(const b200lu_symbolic_view* sym, const b200lu_option
   CU_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_failed), 2 * sizeof(int32_t)));
 
   // destination table, resolved on the device once
-  h->dest16 = S.max_row_len <= 65535;
+  // 16-bit destination offsets unless a row has more than 65 535 entries; B200LU_DEST32=1 forces the 32-bit kernels (test knob)
+  h->dest16 = S.max_row_len <= 65535 && !(std::getenv("B200LU_DEST32") && std::atoi(std::getenv("B200LU_DEST32")) == 1);
   ST_TRY(dev_alloc(h, reinterpret_cast<char**>(&h->d_dest),
                    static_cast<size_t>(S.update_pairs) * (h->dest16 ? 2 : 4) + 16));
   if (n > 0 && S.update_pairs > 0) {

@@ -134,6 +134,28 @@ def test_lu_values_bitwise_on_random_sparse(scaling, amd):
 
 
 @needs_ref
+def test_lu_values_bitwise_with_32_bit_destination_tables(monkeypatch):
+    """factor_kernel<uint32_t, ...>: the destination table of patterns with rows of more than 65 535 entries, forced
+    here (B200LU_DEST32=1) on random patterns and on a KKT sequence."""
+    monkeypatch.setenv("B200LU_DEST32", "1")
+    rng = rb.RefRng(97)
+    for _ in range(12):
+        A = rng.random_sparse(rng.uniform_int(2, 80), 5, 0.1, 1.0, True)
+        fx = csr_fixture(A, False, True)
+        f = rlu.factorize(fx.sym, fx.matrix())
+        expect, failed = fx.oracle.factorize(fx.values[0])
+        assert failed == -1 and np.array_equal(f.values, expect)
+        f.close()
+    fx = kkt_fixture(1400, 600, num_systems=2)
+    f = rlu.NumericFactors(fx.sym)
+    for k in range(2):
+        rlu.refactorize(f, fx.matrix(k))
+        expect, failed = fx.oracle.factorize(fx.values[k])
+        assert failed == -1 and np.array_equal(f.values, expect)
+    f.close()
+
+
+@needs_ref
 def test_refactorize_is_bitwise_identical_to_factorize():
     # test_numeric.cpp:223-253, acceptance.cpp:190-205
     rng = rb.RefRng(93)
