@@ -205,7 +205,12 @@ b200lu_status launch_scatter(H* h) {
 
 b200lu_status launch_factor(H* h, int64_t* failed_row) {
   if (failed_row) *failed_row = -1;
-  if (h->n == 0) return B200LU_OK;
+  if (h->n == 0) {  // src/numeric.cpp:34-57 on an empty pattern: no row can fail; the factors become valid, the generation advances
+    h->scattered = false;
+    h->valid = true;
+    ++h->generation;
+    return B200LU_OK;
+  }
   arm_factor_kernel<<<1, 1, 0, h->stream>>>(h->d_counters, h->d_failed);
   ST_TRY(check_launch(h, "arm_factor_kernel"));
   if (!h->sched.trivial_rows.empty()) {

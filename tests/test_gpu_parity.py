@@ -155,6 +155,33 @@ def test_lu_values_bitwise_with_32_bit_destination_tables(monkeypatch):
     f.close()
 
 
+def test_empty_system_follows_the_reference_conventions():
+    """A 0 x 0 system: eliminate (src/numeric.cpp:27-58) has no row that could fail, so the factors become valid and the
+    generation advances; solve_system returns an empty x; fgmres_refine sees ||r|| / max(||b||, 1 if b = 0) = 0 <= tol and
+    returns after 0 iterations, converged, history [0] (src/refine.cpp:51-58, src/sparse.cpp:283-288). Single handle and batch."""
+    from paper_2306_14337_b200 import analysis
+    from paper_2306_14337_b200.batch import BatchedFactors
+    A = rlu.CsrMatrix(0, 0, np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int64), np.zeros(0))
+    sym = analysis.symbolic_analyze(A)
+    assert sym.n == 0 and sym.col_indices.size == 0
+    f = rlu.factorize(sym, A)
+    assert f.valid and f.generation == 1 and f.values.size == 0
+    rlu.refactorize(f, A)
+    assert f.valid and f.generation == 2
+    x = rlu.solve_system(f, np.zeros(0))
+    assert x.shape == (0,)
+    out = rlu.fgmres_refine(f, np.zeros(0), x)
+    assert out.iterations == 0 and out.converged and list(out.residual_history) == [0.0]
+    f.close()
+    bf = BatchedFactors(sym, 3)
+    bf.refactorize(np.zeros((3, 0)))
+    xs = bf.solve_system(np.zeros((3, 0)))
+    assert tuple(xs.shape) == (3, 0)
+    _, outs = bf.fgmres_refine(np.zeros((3, 0)), xs, rlu.RefineConfig())
+    assert [(o.iterations, bool(o.converged)) for o in outs] == [(0, True)] * 3
+    bf.close()
+
+
 @needs_ref
 def test_refactorize_is_bitwise_identical_to_factorize():
     # test_numeric.cpp:223-253, acceptance.cpp:190-205
