@@ -216,6 +216,37 @@ def test_batch_32_bit_destination_tables(team, monkeypatch):
 
 
 @needs_ref
+def test_batch_zero_right_hand_side_in_one_scenario():
+    """b = 0 for ONE scenario of a batch: its solution is exactly zero, relative_residual uses the denominator 1
+    (src/sparse.cpp:283-288), fgmres_refine returns after 0 iterations, converged (src/refine.cpp:51-58) — while its
+    neighbours in the same warp refine as usual; every scenario against the oracle."""
+    fx = kkt_fixture(700, 300, num_systems=3)
+    batch = 6
+    vals, rhs = _scenarios(fx, batch)
+    rhs[1] = 0.0
+    rhs[4] = 0.0
+    f = BatchedFactors(fx.sym, batch)
+    try:
+        f.refactorize(vals)
+        x = f.solve_system(rhs)
+        assert not np.any(x[1]) and not np.any(x[4])
+        rr = f.relative_residual(x, rhs)
+        assert rr[1] == 0.0 and rr[4] == 0.0
+        xr, outcomes = f.fgmres_refine(rhs, x)
+        for s in range(batch):
+            lu, _ = fx.oracle.factorize(vals[s])
+            A = fx.oracle_csr(0, vals[s])
+            x_ref, its_ref, conv_ref, hist_ref = ob.refine(A, rhs[s], x[s], fx.oracle, lu)
+            assert outcomes[s].iterations == its_ref and outcomes[s].converged == conv_ref
+            assert len(outcomes[s].residual_history) == len(hist_ref)
+            assert A.relative_residual(xr[s], rhs[s]) <= max(4 * A.relative_residual(x_ref, rhs[s]), 1e-15)
+        assert outcomes[1].iterations == 0 and outcomes[1].converged and list(outcomes[1].residual_history) == [0.0]
+        assert not np.any(xr[1])
+    finally:
+        f.close()
+
+
+@needs_ref
 @pytest.mark.parametrize("contexts", [2, 4, 8])
 def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
     """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
