@@ -247,6 +247,46 @@ def test_batch_zero_right_hand_side_in_one_scenario():
 
 
 @needs_ref
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_batch_non_finite_input_stays_in_its_scenario(bad):
+    """A NaN / Inf among the values of ONE scenario: the reference neither fails (fabs(NaN) <= floor is false,
+    src/numeric.cpp:48) nor stops; here nothing may hang on it (x is its own ready flag in the sweeps: a computed NaN
+    is canonicalised, never mistaken for the pending marker), the scenario's factors carry NaN exactly where the
+    oracle's do, refinement reports non-convergence, and the other scenarios of the same warp stay bit-exact."""
+    fx = kkt_fixture(700, 300, num_systems=3)
+    vals = np.stack([fx.values[s % 3].copy() for s in range(5)])
+    rhs = np.stack([fx.rhs[s % 3] for s in range(5)])
+    vals[2, 17] = bad
+    vals[2, vals.shape[1] // 2] = bad
+    f = BatchedFactors(fx.sym, 5)
+    try:
+        f.refactorize(vals)
+        x = f.solve_system(rhs)
+        _, outs = f.fgmres_refine(rhs, x, rlu.RefineConfig(5, 1e-14))
+        for s in (0, 1, 3, 4):
+            ref, failed = fx.oracle.factorize(vals[s])
+            assert np.array_equal(f.values(s), ref)
+            assert np.array_equal(x[s], fx.oracle.solve_system(ref, rhs[s])[0])
+            assert outs[s].converged
+        ref, failed = fx.oracle.factorize(vals[2])
+        got = f.values(2)
+        assert failed == -1 and f.valid(2)
+        assert np.array_equal(np.isnan(got), np.isnan(ref)) and np.isnan(got).any()
+        assert np.array_equal(got[~np.isnan(got)], ref[~np.isnan(ref)])
+        assert not outs[2].converged and outs[2].iterations == 5
+    finally:
+        f.close()
+    g = rlu.NumericFactors(fx.sym)
+    A0 = fx.matrix(0)
+    rlu.refactorize(g, rlu.CsrMatrix(fx.n, fx.n, A0.row_offsets, A0.col_indices, vals[2]))
+    assert g.valid and np.array_equal(np.isnan(g.values), np.isnan(ref))
+    out = rlu.fgmres_refine(g, rhs[2], rlu.solve_system(g, rhs[2]), rlu.RefineConfig(5, 1e-14))
+    assert not out.converged
+    g.close()
+
+
+@needs_ref
 @pytest.mark.parametrize("contexts", [2, 4, 8])
 def test_batch_multi_context_row_blocks_are_bit_exact(contexts, monkeypatch):
     """The experimental non-blocking form of the row-blocked kernel (csrc/blockmc.cuh: W block contexts per warp,
