@@ -183,6 +183,40 @@ def test_empty_system_follows_the_reference_conventions():
 
 
 @needs_ref
+def test_handles_on_different_patterns_coexist():
+    """Distinct instances may live side by side (include/rlu/numeric.hpp:19-21). The dynamic shared-memory limit of a
+    kernel is per FUNCTION, process-wide: a handle created later on a smaller pattern (shorter tail rows, no wide rows)
+    must not lower it under a live handle with a larger one. Large, small, batch handle of a third pattern, then the
+    large one again — every result against the oracle."""
+    from paper_2306_14337_b200.batch import BatchedFactors
+    big = kkt_fixture(6300, 2700, num_systems=2)
+    small = csr_fixture(rb.RefRng(7).random_sparse(30, 4, 0.1, 1.0, True), False, True)
+    mid = kkt_fixture(700, 300, num_systems=2)
+    fb = rlu.NumericFactors(big.sym, rlu.FactorOptions(strict_order=True))
+    rlu.refactorize(fb, big.matrix(0))
+    fs = rlu.NumericFactors(small.sym, rlu.FactorOptions(strict_order=True))
+    rlu.refactorize(fs, small.matrix())
+    bm = BatchedFactors(mid.sym, 5)
+    bm.refactorize(np.stack([mid.values[s % 2] for s in range(5)]))
+    for k in (1, 0):
+        rlu.refactorize(fb, big.matrix(k))
+        ref, failed = big.oracle.factorize(big.values[k])
+        assert failed == -1 and np.array_equal(fb.values, ref)
+        assert np.array_equal(rlu.solve_system(fb, big.rhs[k]), big.oracle.solve_system(ref, big.rhs[k])[0])
+        out = rlu.fgmres_refine(fb, big.rhs[k], rlu.solve_system(fb, big.rhs[k]))
+        assert out.converged
+    ref_s, _ = small.oracle.factorize(small.values[0])
+    assert np.array_equal(fs.values, ref_s)
+    assert np.array_equal(rlu.solve_system(fs, small.rhs[0]), small.oracle.solve_system(ref_s, small.rhs[0])[0])
+    ref_m, _ = mid.oracle.factorize(mid.values[1])
+    assert np.array_equal(bm.values(3), ref_m)
+    xm = bm.solve_system(np.stack([mid.rhs[s % 2] for s in range(5)]))
+    assert np.array_equal(xm[3], mid.oracle.solve_system(ref_m, mid.rhs[1])[0])
+    for h in (fb, fs, bm):
+        h.close()
+
+
+@needs_ref
 def test_refactorize_is_bitwise_identical_to_factorize():
     # test_numeric.cpp:223-253, acceptance.cpp:190-205
     rng = rb.RefRng(93)
