@@ -558,6 +558,60 @@ def test_staged_pipeline_takes_device_buffers():
         g.close()
 
 
+def test_staged_calls_reject_misuse_and_report_zero_pivots():
+    """The staged submission calls outside their protocol: nothing staged, a third set while two are pending (the handle
+    stays usable), and a singular scenario inside a staged batch (per-scenario failed rows, neighbours factorized and
+    solved — as through the plain calls, tests/test_numeric.cpp:173-184 inside a batch)."""
+    fx = golden_fixture("kkt_small")
+    batch = 5
+    vals, rhs = _scenarios(fx, batch)
+    f = BatchedFactors(fx.sym, batch)
+    g = BatchedFactors(fx.sym, batch)
+    try:
+        with pytest.raises(rlu.Error, match="no staged values"):
+            f.refactorize_staged()
+        out = np.empty((batch, fx.n))
+        with pytest.raises(rlu.Error):
+            f.solve_refine_staged(out)  # neither factors nor staged right-hand sides
+        f.stage_inputs(vals, rhs)
+        f.stage_inputs(vals * 1.5, rhs * 0.5)
+        with pytest.raises(rlu.Error, match="not been consumed"):
+            f.stage_inputs(vals, rhs)
+        outs = [np.empty((batch, fx.n)) for _ in range(2)]
+        for k in range(2):  # both pending sets are still consumed in order
+            f.refactorize_staged()
+            f.solve_refine_staged(outs[k])
+        f.staged_wait()
+        for k, (v, b) in enumerate(((vals, rhs), (vals * 1.5, rhs * 0.5))):
+            g.refactorize(v)
+            xr, _ = g.fgmres_refine(b, g.solve_system(b))
+            assert np.array_equal(outs[k], xr), k
+    finally:
+        f.close()
+        g.close()
+    good = np.array([[4.0, 1, 0], [1, 4, 1], [0, 1, 4]])
+    bad = np.array([[1.0, 1, 0], [1, 1, 1], [0, 1, 1]])
+    fz = dense_fixture(good)
+    rows = np.repeat(np.arange(3), np.diff(fz.ro))
+    zv = np.stack([m[rows, fz.ci] for m in (good, bad, 2 * good)])
+    zb = np.stack([np.array([1.0, 2.0, 3.0])] * 3)
+    h = BatchedFactors(fz.sym, 3)
+    try:
+        h.stage_inputs(zv, zb)
+        with pytest.raises(rlu.ZeroPivotError) as ei:
+            h.refactorize_staged()
+        assert ei.value.scenarios == [1] and ei.value.rows[1] == fz.oracle.factorize(zv[1])[1]
+        assert h.valid(0) and not h.valid(1) and h.valid(2)
+        failed = h.refactorize(zv, raise_on_zero_pivot=False)
+        assert list(failed) == [-1, ei.value.rows[1], -1]
+        x = h.solve_system(zb)
+        for s in (0, 2):
+            lu, _ = fz.oracle.factorize(zv[s])
+            assert np.array_equal(x[s], fz.oracle.solve_system(lu, zb[s])[0])
+    finally:
+        h.close()
+
+
 def test_staged_pipeline_matches_the_plain_calls_bitwise():
     """The staged (pipelined) submission — inputs of batch k + 1 copied while batch k is processed, solutions
     leaving on their own stream — gives, for every batch of a sequence, exactly the results of the plain
