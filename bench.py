@@ -884,7 +884,7 @@ def run_batch(args):
                 "median_refine_iters": int(statistics.median(r.refine_iters for r in allrecs)),
                 "failed": sum(1 for r in allrecs if r.failed_row >= 0)},
             "roofline": {
-                "kernel": "bfactor_kernel + the trailing launch (bfactor_block_team_kernel: row blocks, one warp per row; bfactor_tile_kernel up to 32 scenarios per GPU) — K2 numeric refactorization, scenario-batched, timed as one", "bound": "hbm",
+                "kernel": "bfactor_kernel + the trailing launch (bfactor_block_team_kernel: row blocks, one warp per row, pivot rows staged by cp.async.bulk on an mbarrier; bfactor_tile_kernel up to 32 scenarios per GPU) — K2 numeric refactorization, scenario-batched, timed as one", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": ab["eliminate"], "avg_launch_ms": fac_avg_ms,
