@@ -125,9 +125,13 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            phys = int(vis.split(",")[device_index]) if vis and vis.split(",")[device_index].isdigit() else device_index
-            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            # the CUDA ordinal -> the NVML device: CUDA_VISIBLE_DEVICES may renumber (indices) or name (UUIDs) the devices
+            vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+            ent = vis[device_index] if device_index < len(vis) else str(device_index)
+            if ent.isdigit():
+                h = pynvml.nvmlDeviceGetHandleByIndex(int(ent))
+            else:
+                h = pynvml.nvmlDeviceGetHandleByUUID(ent.encode() if hasattr(ent, "encode") else ent)
             smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
